@@ -1,0 +1,178 @@
+/*
+ * stencil_b200.h -- C ABI of the B200-native stencil sweep library
+ * (paper_1004_1741_b200/libsb200.so).
+ *
+ * Drop-in boundary for the reference package `stencilbench`
+ * (arxiv 1004.1741).  The reference has no FFI of its own: its hot path is
+ * the Python entry `sweeps.run(plan, g)` (pkg/src/stencilbench/sweeps/
+ * __init__.py:52-71) dispatching to engines that call numba plane-window
+ * kernels.  Each entry point below replaces one engine (see INTEGRATION.md
+ * for the ctypes binding a maintainer adds on the reference side):
+ *
+ *   sb_jacobi / sb_run_host(JACOBI)  <- run_serial / run_threaded_jacobi /
+ *                                       run_wavefront_jacobi
+ *                                       (sweeps/serial.py:8-42,
+ *                                        sweeps/threaded.py:28-59,
+ *                                        sweeps/wavefront.py:133-137,160-312)
+ *   sb_gs / sb_run_host(GS_*)        <- run_serial / run_pipeline_gs /
+ *                                       run_wavefront_gs (GS kernels)
+ *                                       (sweeps/threaded.py:62-96,
+ *                                        sweeps/wavefront.py:139-143,315-376)
+ *   sb_jacobi_slabs / sb_jacobi_planes / sb_slab_layout
+ *                                    <- run_threaded_jacobi's k-slab split
+ *                                       (sweeps/threaded.py:28-59, :39)
+ *                                       across GPUs (z-slabs + halo exchange)
+ *
+ * Grid layout (reference grid.py:61-91): (nk+2) x (nj+2) x (ni+2) doubles,
+ * C order, i unit stride; interior cell (k,j,i) at padded (k+1,j+1,i+1);
+ * halo cells are Dirichlet data and are never written.
+ *
+ * Arithmetic (reference kernels.py:125-187): bitwise identical to the
+ * reference for every entry point and every depth --
+ *   Jacobi:          a*c + b*(((((W+E)+S)+N)+D)+U)
+ *   GS naive:        b*(((((W+E)+S)+N)+D)+U)            in lexicographic order
+ *   GS interleaved:  b*(W + ((((E+S)+N)+D)+U))          in lexicographic order
+ *
+ * Errors: every function returns an sb_status; 0 is success.  Argument
+ * errors are detected before any device work (like the reference's
+ * PlanError / PartitionError, raised before threads start).  The message of
+ * the last error on the calling thread is sb_last_error().
+ *
+ * Threading: calls are synchronous with respect to `stream` only when the
+ * function says so; device-pointer entry points enqueue work on `stream`
+ * (a cudaStream_t, NULL = legacy default stream) and return.  Not
+ * reentrant across threads for the same buffers.
+ */
+#ifndef STENCIL_B200_H
+#define STENCIL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SB_OK = 0,
+    SB_ERR_DIMENSION = 1,  /* -> DimensionError (grid extents)            */
+    SB_ERR_PLAN = 2,       /* -> PlanError (iters < 0, bad kernel/depth)   */
+    SB_ERR_CONFIG = 3,     /* -> ConfigError                                */
+    SB_ERR_PARTITION = 4,  /* -> PartitionError (more slabs than planes)   */
+    SB_ERR_CUDA = 5,       /* -> DeviceError (CUDA runtime/launch failure)  */
+    SB_ERR_TIMEOUT = 6,    /* -> DeviceError (inter-CTA flag wait expired)  */
+    SB_ERR_ARGUMENT = 7,   /* -> ValueError (null/misaligned pointer)       */
+    SB_ERR_NODEVICE = 8    /* -> DeviceError (no CUDA device)               */
+} sb_status;
+
+typedef enum {
+    SB_KERNEL_JACOBI = 0,
+    SB_KERNEL_GS_NAIVE = 1,
+    SB_KERNEL_GS_INTERLEAVED = 2
+} sb_kernel;
+
+/* Library/ABI version (major*10000 + minor*100 + patch). */
+int sb_version(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* sb_last_error(void);
+
+/* Number of visible CUDA devices (0 when none). */
+int sb_device_count(void);
+
+/* Maximum temporal block depth supported by sb_jacobi. */
+int sb_max_depth(void);
+
+/*
+ * Jacobi sweeps on device memory.  `grid` and `scratch` are device
+ * pointers to two distinct padded grids; `scratch` needs no initialisation
+ * (its halo is copied from `grid` on the stream).  Advances `iters` sweeps,
+ * fusing up to `depth` (1..sb_max_depth()) sweeps per HBM pass; iters that
+ * are not a multiple of depth end with shallower passes.  On return
+ * *result_in_scratch tells which buffer holds the final field (the other
+ * holds an intermediate one), like run_serial returning the copy for odd
+ * iteration counts.  Asynchronous on `stream`.
+ */
+int sb_jacobi(double* grid, double* scratch, int64_t ni, int64_t nj, int64_t nk,
+              int64_t iters, double a, double b, int depth, void* stream,
+              int* result_in_scratch);
+
+/*
+ * Lexicographic Gauss-Seidel sweeps, in place on the device grid.
+ * kernel: SB_KERNEL_GS_NAIVE or SB_KERNEL_GS_INTERLEAVED (selects the
+ * association, bitwise equal to the matching reference kernel).
+ * Asynchronous on `stream`.
+ */
+int sb_gs(double* grid, int64_t ni, int64_t nj, int64_t nk, int64_t iters, double b,
+          int kernel, void* stream);
+
+/*
+ * Wait for all work queued on `stream` and report deferred failures: a
+ * CUDA error raised by the kernels, or SB_ERR_TIMEOUT when a Gauss-Seidel
+ * inter-CTA dependency wait expired (the kernel then bails out instead of
+ * hanging and the grid content is unspecified).
+ */
+int sb_sync(void* stream);
+
+/*
+ * Host-buffer entry point: the whole reference `run` contract in one call.
+ * host_grid: padded grid in host memory (pinned or pageable), updated in
+ * place with the final field.  Copies to device `device`, sweeps, copies
+ * back; synchronous.  For Jacobi a = centre weight, depth as in sb_jacobi;
+ * for GS a and depth are ignored.
+ */
+int sb_run_host(int kernel, double* host_grid, int64_t ni, int64_t nj, int64_t nk,
+                int64_t iters, double a, double b, int depth, int device);
+
+/*
+ * Pinned host allocation for grids (so sb_run_host copies at full PCIe
+ * rate).  Returns NULL on failure.
+ */
+double* sb_host_alloc(int64_t count);
+void sb_host_free(double* p);
+
+/*
+ * One block of `sweeps` (1..sb_max_depth()) fused Jacobi sweeps src -> dst
+ * that writes only the output planes [k_out_lo, k_out_hi) (padded plane
+ * indices within [1, nk]); every other plane of dst is left untouched.
+ * The building block of the z-slab decomposition: a slab computes the
+ * planes its neighbours need first, then its interior while those travel.
+ * Values are exact wherever the input is valid `sweeps` planes beyond the
+ * output range.  Asynchronous on `stream`.
+ */
+int sb_jacobi_planes(const double* src, double* dst, int64_t ni, int64_t nj, int64_t nk,
+                     int64_t k_out_lo, int64_t k_out_hi, int sweeps, double a, double b,
+                     void* stream);
+
+/*
+ * Layout of slab `slab` of the z-slab decomposition of nk interior planes
+ * into `nslabs` slabs (partition_blocks semantics, sweeps/plan.py:106-120):
+ * it owns global padded planes [*own_lo, *own_hi) and stores *ghost_lo
+ * planes below and *ghost_hi above them (`depth` toward a neighbour slab, 1
+ * -- the Dirichlet halo plane -- at the global boundary).  The slab buffer
+ * is therefore a padded grid of (own_hi-own_lo + ghost_lo + ghost_hi)
+ * planes holding global planes [own_lo-ghost_lo, own_hi+ghost_hi).
+ * SB_ERR_PARTITION when nslabs > nk or an inner slab owns < depth planes.
+ */
+int sb_slab_layout(int64_t nk, int nslabs, int slab, int depth, int64_t* own_lo, int64_t* own_hi,
+                   int64_t* ghost_lo, int64_t* ghost_hi);
+
+/*
+ * Multi-slab Jacobi in one process: slabs[s] / scratch[s] are device
+ * buffers on devices[s] laid out per sb_slab_layout (slabs[s] filled with
+ * the initial field including ghosts; scratch[s] needs no initialisation),
+ * streams[s] a stream on devices[s].  Runs `iters` sweeps, `depth` per halo
+ * exchange (peer copies over NVLink between GPUs, device copies between
+ * slabs sharing a GPU), overlapping each exchange with the slab interiors.
+ * Synchronous.  *result_in_scratch tells which buffer set holds the result
+ * (owned planes exact; ghost planes are not meaningful afterwards).
+ */
+int sb_jacobi_slabs(int nslabs, const int* devices, double* const* slabs,
+                    double* const* scratch, int64_t ni, int64_t nj, int64_t nk,
+                    int64_t iters, double a, double b, int depth, void* const* streams,
+                    int* result_in_scratch);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STENCIL_B200_H */

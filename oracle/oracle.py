@@ -1,0 +1,88 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes wrapper of the CPU oracle
+(oracle/sb_oracle.c, a plain-C restatement of the reference sweeps).
+
+Used by tests/ (as the parity checker), __graft_entry__.smoke() (checker)
+and bench.py (cpu_baseline leg and ``--impl reference``).  The product
+package never imports this module.
+
+Pinned against the reference: tests/test_oracle.py compares every entry
+point bit for bit with tests/golden/ (fixtures produced by the reference
+package itself, tests/golden/make_golden.py).
+"""
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB = HERE / "libsb_oracle.so"
+
+KERNEL_IDS = {"jacobi": 0, "gs-naive": 1, "gs-interleaved": 2}
+
+_lib = None
+
+
+def build():
+    subprocess.run(["make", "-C", str(HERE), "-s"], check=True)
+
+
+def load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB.exists():
+        build()
+    lib = ctypes.CDLL(str(LIB))
+    i64, dbl, vp, i32 = ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_int
+    lib.sbo_run_serial.argtypes = [i32, vp, vp, i64, i64, i64, i64, dbl, dbl]
+    lib.sbo_run_serial.restype = i32
+    lib.sbo_run_threaded_jacobi.argtypes = [vp, vp, i64, i64, i64, i64, dbl, dbl, i32]
+    lib.sbo_run_threaded_jacobi.restype = i32
+    lib.sbo_run_pipeline_gs.argtypes = [i32, vp, i64, i64, i64, i64, dbl, i32]
+    lib.sbo_run_pipeline_gs.restype = i32
+    _lib = lib
+    return lib
+
+
+def _check(arr):
+    if not (arr.dtype == np.float64 and arr.flags.c_contiguous and arr.ndim == 3):
+        raise ValueError("oracle grids are C-contiguous float64 (nk+2, nj+2, ni+2) arrays")
+    nk, nj, ni = (s - 2 for s in arr.shape)
+    return ni, nj, nk
+
+
+def run_serial(kernel, data, iters, a=0.0, b=1.0 / 6.0):
+    """Serial reference sweeps (sweeps/serial.py:8-42).  Returns a new array
+    holding the final field; `data` is not modified."""
+    g = np.array(data, dtype=np.float64, order="C", copy=True)
+    ni, nj, nk = _check(g)
+    scratch = np.empty_like(g) if kernel == "jacobi" else g
+    in_s = load().sbo_run_serial(KERNEL_IDS[kernel], g.ctypes.data, scratch.ctypes.data,
+                                 ni, nj, nk, iters, a, b)
+    return scratch if in_s else g
+
+
+def run_threaded(kernel, data, iters, a=0.0, b=1.0 / 6.0, threads=None):
+    """Threaded Jacobi (k-slabs, threaded.py:28-59) or pipeline GS
+    (j-blocks, threaded.py:62-96) on `threads` host threads.  Bitwise equal
+    to run_serial.  Returns a new array holding the final field."""
+    threads = threads or os.cpu_count() or 1
+    g = np.array(data, dtype=np.float64, order="C", copy=True)
+    ni, nj, nk = _check(g)
+    lib = load()
+    if kernel == "jacobi":
+        threads = max(1, min(threads, nk))
+        scratch = np.empty_like(g)
+        in_s = lib.sbo_run_threaded_jacobi(g.ctypes.data, scratch.ctypes.data, ni, nj, nk, iters,
+                                           a, b, threads)
+        if in_s < 0:
+            raise ValueError("partition error")
+        return scratch if in_s else g
+    threads = max(1, min(threads, nj))
+    rc = lib.sbo_run_pipeline_gs(KERNEL_IDS[kernel], g.ctypes.data, ni, nj, nk, iters, b, threads)
+    if rc < 0:
+        raise ValueError("partition error")
+    return g

@@ -1,0 +1,272 @@
+// host.cu -- host-buffer entry point and the z-slab decomposition driver.
+//
+// sb_run_host is the whole reference `sweeps.run(plan, g)` contract in one
+// synchronous call on host memory (the numpy path of the Python drop-in).
+//
+// The z-slab functions are the multi-GPU form of the reference's k-slab
+// threading (sweeps/threaded.py:28-59, partition_blocks at :39): slab s owns
+// the contiguous interior planes partition_blocks(nk, nslabs)[s] and keeps
+// `depth` ghost planes per inner side, so `depth` fused sweeps can run
+// between two halo exchanges (the overlapped-halo form of the paper's
+// per-time-block exchange).  Each period computes the ghost-feeding edge
+// planes first, then the slab interior while the edges travel to the
+// neighbours (cudaMemcpyPeerAsync over NVLink, or a device copy when two
+// slabs share a GPU).  Results are bitwise identical to the single-grid run.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/stencil_b200.h"
+#include "sb_internal.h"
+
+namespace sb {
+int jacobi_block(const double* src, double* dst, int ni, int nj, int nk, int kfirst, int klast,
+                 int T, double a, double b, cudaStream_t st);
+int gs_check_error(cudaStream_t st);
+
+// cached device buffers + stream per device for sb_run_host
+struct HostCtx {
+    double* g = nullptr;
+    double* s = nullptr;
+    size_t cap = 0;  // doubles per buffer
+    cudaStream_t st = nullptr;
+};
+static std::mutex g_host_mu;
+static HostCtx g_host[64];
+
+// partition_blocks semantics (reference sweeps/plan.py:106-120)
+static void part(int64_t extent, int count, int idx, int64_t* lo, int64_t* hi) {
+    const int64_t base = extent / count, rem = extent % count;
+    *lo = idx * base + std::min<int64_t>(idx, rem);
+    *hi = *lo + base + (idx < rem ? 1 : 0);
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+int sb_run_host(int kernel, double* host_grid, int64_t ni, int64_t nj, int64_t nk, int64_t iters,
+                double a, double b, int depth, int device) {
+    clear_error();
+    int rc = check_dims(ni, nj, nk);
+    if (rc) return rc;
+    if (iters < 0) return fail(SB_ERR_PLAN, "iter_end must be >= 0, got %lld", (long long)iters);
+    if (kernel < SB_KERNEL_JACOBI || kernel > SB_KERNEL_GS_INTERLEAVED)
+        return fail(SB_ERR_PLAN, "unknown kernel %d", kernel);
+    if (kernel == SB_KERNEL_JACOBI && (depth < 1 || depth > sb_max_depth()))
+        return fail(SB_ERR_PLAN, "depth must be in [1, %d], got %d", sb_max_depth(), depth);
+    if (!host_grid) return fail(SB_ERR_ARGUMENT, "null pointer");
+    if (iters == 0) return SB_OK;
+    int ndev = sb_device_count();
+    if (ndev < 1) return fail(SB_ERR_NODEVICE, "no CUDA device");
+    if (device < 0 || device >= ndev || device >= 64)
+        return fail(SB_ERR_ARGUMENT, "device %d out of range (%d visible)", device, ndev);
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    HostCtx& H = g_host[device];
+    const size_t count = size_t(ni + 2) * size_t(nj + 2) * size_t(nk + 2);
+    const size_t bytes = count * sizeof(double);
+    if (!H.st && (e = cudaStreamCreateWithFlags(&H.st, cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_fail(e, "cudaStreamCreate");
+    const bool two = (kernel == SB_KERNEL_JACOBI);
+    if (H.cap < count || (two && !H.s)) {
+        if (H.g) cudaFree(H.g);
+        if (H.s) cudaFree(H.s);
+        H.g = H.s = nullptr;
+        H.cap = 0;
+        if ((e = cudaMalloc(&H.g, bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(grid)");
+        if (two && (e = cudaMalloc(&H.s, bytes)) != cudaSuccess) {
+            cudaFree(H.g);
+            H.g = nullptr;
+            return cuda_fail(e, "cudaMalloc(scratch)");
+        }
+        H.cap = count;
+    }
+    if ((e = cudaMemcpyAsync(H.g, host_grid, bytes, cudaMemcpyHostToDevice, H.st)) != cudaSuccess)
+        return cuda_fail(e, "H2D copy");
+    const double* result = H.g;
+    if (kernel == SB_KERNEL_JACOBI) {
+        int in_s = 0;
+        rc = sb_jacobi(H.g, H.s, ni, nj, nk, iters, a, b, depth, H.st, &in_s);
+        if (rc) return rc;
+        result = in_s ? H.s : H.g;
+    } else {
+        rc = sb_gs(H.g, ni, nj, nk, iters, b, kernel, H.st);
+        if (rc) return rc;
+    }
+    if ((e = cudaMemcpyAsync(host_grid, result, bytes, cudaMemcpyDeviceToHost, H.st)) != cudaSuccess)
+        return cuda_fail(e, "D2H copy");
+    if ((e = cudaStreamSynchronize(H.st)) != cudaSuccess) return cuda_fail(e, "sweep execution");
+    if (kernel != SB_KERNEL_JACOBI) return gs_check_error(H.st);
+    return SB_OK;
+}
+
+int sb_jacobi_planes(const double* src, double* dst, int64_t ni, int64_t nj, int64_t nk,
+                     int64_t k_out_lo, int64_t k_out_hi, int sweeps, double a, double b,
+                     void* stream) {
+    clear_error();
+    int rc = check_dims(ni, nj, nk);
+    if (rc) return rc;
+    if (sweeps < 1 || sweeps > sb_max_depth())
+        return fail(SB_ERR_PLAN, "sweeps per block must be in [1, %d], got %d", sb_max_depth(), sweeps);
+    if (k_out_lo < 1 || k_out_hi > nk + 1 || k_out_lo > k_out_hi)
+        return fail(SB_ERR_ARGUMENT, "output planes [%lld, %lld) outside [1, %lld]", (long long)k_out_lo,
+                    (long long)k_out_hi, (long long)nk);
+    if (!src || !dst || src == dst) return fail(SB_ERR_ARGUMENT, "need two distinct buffers");
+    return jacobi_block(src, dst, (int)ni, (int)nj, (int)nk, (int)k_out_lo, (int)k_out_hi, sweeps, a, b,
+                        static_cast<cudaStream_t>(stream));
+}
+
+int sb_slab_layout(int64_t nk, int nslabs, int slab, int depth, int64_t* own_lo, int64_t* own_hi,
+                   int64_t* ghost_lo, int64_t* ghost_hi) {
+    clear_error();
+    if (nslabs < 1 || nslabs > nk)
+        return fail(SB_ERR_PARTITION, "cannot split nk=%lld planes into %d slabs", (long long)nk, nslabs);
+    if (slab < 0 || slab >= nslabs) return fail(SB_ERR_ARGUMENT, "slab %d of %d", slab, nslabs);
+    if (depth < 1 || depth > sb_max_depth()) return fail(SB_ERR_PLAN, "depth %d", depth);
+    int64_t lo, hi;
+    part(nk, nslabs, slab, &lo, &hi);
+    *own_lo = lo + 1;  // padded global plane indices
+    *own_hi = hi + 1;
+    *ghost_lo = (slab == 0) ? 1 : depth;
+    *ghost_hi = (slab == nslabs - 1) ? 1 : depth;
+    if (nslabs > 1 && hi - lo < depth)
+        return fail(SB_ERR_PARTITION, "slab %d owns %lld planes, fewer than depth %d", slab,
+                    (long long)(hi - lo), depth);
+    return SB_OK;
+}
+
+int sb_jacobi_slabs(int nslabs, const int* devices, double* const* slabs, double* const* scratch,
+                    int64_t ni, int64_t nj, int64_t nk, int64_t iters, double a, double b, int depth,
+                    void* const* streams, int* result_in_scratch) {
+    clear_error();
+    int rc = check_dims(ni, nj, nk);
+    if (rc) return rc;
+    if (iters < 0) return fail(SB_ERR_PLAN, "iter_end must be >= 0, got %lld", (long long)iters);
+    if (!devices || !slabs || !scratch || !streams || !result_in_scratch)
+        return fail(SB_ERR_ARGUMENT, "null pointer");
+    struct Slab {
+        int dev;
+        double* buf[2];
+        cudaStream_t st, comm;
+        int64_t own_lo, own_hi, glo, ghi, nkl;  // nkl: local interior planes
+        cudaEvent_t edge, start, sent_up, sent_dn;
+    };
+    std::vector<Slab> S(nslabs);
+    for (int s = 0; s < nslabs; ++s) {
+        if ((rc = sb_slab_layout(nk, nslabs, s, depth, &S[s].own_lo, &S[s].own_hi, &S[s].glo, &S[s].ghi)))
+            return rc;
+        S[s].dev = devices[s];
+        S[s].buf[0] = slabs[s];
+        S[s].buf[1] = scratch[s];
+        S[s].st = static_cast<cudaStream_t>(streams[s]);
+        S[s].nkl = (S[s].own_hi - S[s].own_lo) + S[s].glo + S[s].ghi - 2;
+        if (!slabs[s] || !scratch[s] || slabs[s] == scratch[s])
+            return fail(SB_ERR_ARGUMENT, "slab %d needs two distinct buffers", s);
+    }
+    *result_in_scratch = 0;
+    if (iters == 0) return SB_OK;
+    const int64_t nip = ni + 2, plane = nip * (nj + 2);
+    const size_t pbytes = size_t(plane) * sizeof(double);
+    cudaError_t e;
+    // streams/events; peer access where the slabs live on different GPUs
+    for (int s = 0; s < nslabs; ++s) {
+        if ((e = cudaSetDevice(S[s].dev)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+        for (int t = 0; t < nslabs; ++t)
+            if (S[t].dev != S[s].dev) {
+                int can = 0;
+                cudaDeviceCanAccessPeer(&can, S[s].dev, S[t].dev);
+                if (can) {
+                    e = cudaDeviceEnablePeerAccess(S[t].dev, 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                    else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+                }
+            }
+        if ((e = cudaStreamCreateWithFlags(&S[s].comm, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(e, "cudaStreamCreate");
+        for (cudaEvent_t* ev : {&S[s].edge, &S[s].start, &S[s].sent_up, &S[s].sent_dn})
+            if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(e, "cudaEventCreate");
+        // both buffers must carry the Dirichlet halo (and the initial ghosts)
+        if ((rc = halo_copy(S[s].buf[0], S[s].buf[1], (int)ni, (int)nj, (int)S[s].nkl, S[s].st))) return rc;
+    }
+    int cur = 0;  // buffer index holding the current field
+    bool first = true;
+    for (int64_t done = 0; done < iters;) {
+        const int T = (int)std::min<int64_t>(depth, iters - done);
+        // 1. per slab: edge planes, then interior
+        for (int s = 0; s < nslabs; ++s) {
+            Slab& X = S[s];
+            cudaSetDevice(X.dev);
+            if (!first) {  // last period's incoming/outgoing copies must be done
+                if (s > 0) cudaStreamWaitEvent(X.st, S[s - 1].sent_up, 0);
+                if (s + 1 < nslabs) cudaStreamWaitEvent(X.st, S[s + 1].sent_dn, 0);
+                cudaStreamWaitEvent(X.st, X.sent_up, 0);
+                cudaStreamWaitEvent(X.st, X.sent_dn, 0);
+            }
+            cudaEventRecord(X.start, X.st);
+            const double* src = X.buf[cur];
+            double* dst = X.buf[cur ^ 1];
+            const int64_t lo = X.glo, hi = X.glo + (X.own_hi - X.own_lo);  // owned, local padded
+            const int64_t elo = (s > 0) ? std::min<int64_t>(lo + depth, hi) : lo;
+            const int64_t ehi = (s + 1 < nslabs) ? std::max<int64_t>(hi - depth, elo) : hi;
+            if (s > 0 && (rc = jacobi_block(src, dst, (int)ni, (int)nj, (int)X.nkl, (int)lo, (int)elo, T, a, b, X.st)))
+                return rc;
+            if (s + 1 < nslabs &&
+                (rc = jacobi_block(src, dst, (int)ni, (int)nj, (int)X.nkl, (int)ehi, (int)hi, T, a, b, X.st)))
+                return rc;
+            cudaEventRecord(X.edge, X.st);
+            if ((rc = jacobi_block(src, dst, (int)ni, (int)nj, (int)X.nkl, (int)elo, (int)ehi, T, a, b, X.st)))
+                return rc;
+        }
+        // 2. exchange: top `depth` owned planes up, bottom `depth` owned planes down
+        for (int s = 0; s < nslabs; ++s) {
+            Slab& X = S[s];
+            cudaSetDevice(X.dev);
+            double* xd = X.buf[cur ^ 1];
+            const int64_t hi = X.glo + (X.own_hi - X.own_lo);
+            if (s + 1 < nslabs) {
+                Slab& Y = S[s + 1];
+                cudaStreamWaitEvent(X.comm, X.edge, 0);
+                cudaStreamWaitEvent(X.comm, Y.start, 0);
+                // X planes [hi-depth, hi) -> Y local planes [0, depth)
+                e = cudaMemcpyPeerAsync(Y.buf[cur ^ 1], Y.dev, xd + (hi - depth) * plane, X.dev,
+                                        depth * pbytes, X.comm);
+                if (e != cudaSuccess) return cuda_fail(e, "halo exchange (up)");
+                cudaEventRecord(X.sent_up, X.comm);
+            }
+            if (s > 0) {
+                Slab& Y = S[s - 1];
+                cudaStreamWaitEvent(X.comm, X.edge, 0);
+                cudaStreamWaitEvent(X.comm, Y.start, 0);
+                // X planes [glo, glo+depth) -> Y local planes [Y.hi, Y.hi+depth)
+                const int64_t yhi = Y.glo + (Y.own_hi - Y.own_lo);
+                e = cudaMemcpyPeerAsync(Y.buf[cur ^ 1] + yhi * plane, Y.dev, xd + X.glo * plane, X.dev,
+                                        depth * pbytes, X.comm);
+                if (e != cudaSuccess) return cuda_fail(e, "halo exchange (down)");
+                cudaEventRecord(X.sent_dn, X.comm);
+            }
+        }
+        cur ^= 1;
+        first = false;
+        done += T;
+    }
+    for (int s = 0; s < nslabs; ++s) {
+        cudaSetDevice(S[s].dev);
+        if ((e = cudaStreamSynchronize(S[s].comm)) != cudaSuccess) return cuda_fail(e, "exchange");
+        if ((e = cudaStreamSynchronize(S[s].st)) != cudaSuccess) return cuda_fail(e, "slab sweeps");
+        cudaStreamDestroy(S[s].comm);
+        for (cudaEvent_t ev : {S[s].edge, S[s].start, S[s].sent_up, S[s].sent_dn}) cudaEventDestroy(ev);
+    }
+    *result_in_scratch = cur;
+    return SB_OK;
+}
+
+}  // extern "C"

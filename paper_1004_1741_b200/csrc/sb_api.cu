@@ -1,0 +1,385 @@
+// sb_api.cu -- C ABI (include/stencil_b200.h) over the sm_100a kernels.
+//
+// Host-side responsibilities: argument validation (mirroring the reference's
+// PlanError/PartitionError/DimensionError checks, raised before any work),
+// TMA descriptor construction, kernel selection per temporal depth,
+// persistent-grid sizing from the SM count, the Dirichlet-halo copy into the
+// scratch buffer, and the host-buffer entry point used by the Python drop-in.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/stencil_b200.h"
+#include "jacobi_tb.cuh"
+#include "sb_internal.h"
+
+namespace sb {
+
+// ---------------------------------------------------------------------------
+// error state
+static thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(SB_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+void clear_error() { g_err.clear(); }
+const char* last_error() { return g_err.c_str(); }
+
+// ---------------------------------------------------------------------------
+// driver entry point for cuTensorMapEncodeTiled (no -lcuda link dependency)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// 3-D map over a padded grid with a (bw, bh, bd) box.
+int make_grid_map3(CUtensorMap* m, const double* base, int64_t nip, int64_t njp, int64_t nkp,
+                   int bw, int bh, int bd) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(SB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {(cuuint64_t)nip, (cuuint64_t)njp, (cuuint64_t)nkp};
+    cuuint64_t strides[2] = {(cuuint64_t)(nip * 8), (cuuint64_t)(nip * njp * 8)};
+    cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bd};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return SB_OK;
+}
+
+int make_grid_map(CUtensorMap* m, const double* base, int64_t nip, int64_t njp, int64_t nkp,
+                  int bw, int bh) {
+    return make_grid_map3(m, base, nip, njp, nkp, bw, bh, 1);
+}
+
+// ---------------------------------------------------------------------------
+// per-device context: SM count, work counters
+struct DevCtx {
+    int sms = 0;
+    int* counters = nullptr;  // device ints
+};
+static std::mutex g_ctx_mu;
+static std::vector<DevCtx> g_ctx;
+
+int dev_ctx(DevCtx** out) {
+    int dev;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    if ((int)g_ctx.size() <= dev) g_ctx.resize(dev + 1);
+    DevCtx& c = g_ctx[dev];
+    if (!c.counters) {
+        e = cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+        e = cudaMalloc(&c.counters, 64 * sizeof(int));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(counters)");
+    }
+    *out = &c;
+    return SB_OK;
+}
+
+int get_counters(int** counters, int* sms) {
+    DevCtx* c;
+    int rc = dev_ctx(&c);
+    if (rc) return rc;
+    *counters = c->counters;
+    *sms = c->sms;
+    return SB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernels: halo copy and the generic (odd pitch) Jacobi sweep
+
+// Copies every halo (Dirichlet) cell of src into dst.
+__global__ void halo_copy_kernel(const double* __restrict__ src, double* __restrict__ dst, int ni,
+                                 int nj, int nk) {
+    const int64_t nip = ni + 2, njp = nj + 2, plane = nip * njp;
+    // faces: k = 0 and k = nk+1 planes (full), then per interior plane the
+    // j = 0 / nj+1 rows and the i = 0 / ni+1 columns
+    const int64_t n_kfaces = 2 * plane;
+    const int64_t n_rows = (int64_t)nk * 2 * nip;
+    const int64_t n_cols = (int64_t)nk * nj * 2;
+    const int64_t total = n_kfaces + n_rows + n_cols;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t off;
+        if (t < n_kfaces) {
+            off = (t < plane) ? t : (int64_t)(nk + 1) * plane + (t - plane);
+        } else if (t < n_kfaces + n_rows) {
+            int64_t u = t - n_kfaces;
+            int64_t k = 1 + u / (2 * nip), r = u % (2 * nip);
+            int64_t j = (r < nip) ? 0 : nj + 1, i = r % nip;
+            off = k * plane + j * nip + i;
+        } else {
+            int64_t u = t - n_kfaces - n_rows;
+            int64_t k = 1 + u / (2 * nj), r = u % (2 * nj);
+            int64_t j = 1 + r / 2, i = (r & 1) ? ni + 1 : 0;
+            off = k * plane + j * nip + i;
+        }
+        dst[off] = src[off];
+    }
+}
+
+// One plain sweep for grids whose row pitch is not a 16-byte multiple (odd
+// ni), where TMA cannot describe the grid.  Thread per (i, j) column,
+// register z-queue, neighbours through the read-only path.
+__global__ void jacobi_generic_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                      int ni, int nj, int kfirst, int klast, int kchunk, double a,
+                                      double b) {
+    const int i = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = 1 + blockIdx.y * blockDim.y + threadIdx.y;
+    if (i > ni || j > nj) return;
+    const int64_t nip = ni + 2, plane = nip * (nj + 2);
+    const int k0 = kfirst + blockIdx.z * kchunk, k1 = min(k0 + kchunk, klast);
+    const double* s = src + j * nip + i;
+    double d = __ldg(s + (k0 - 1) * plane), c = __ldg(s + k0 * plane);
+    for (int k = k0; k < k1; ++k) {
+        const double* q = s + k * plane;
+        const double u = __ldg(q + plane);
+        dst[k * plane + j * nip + i] =
+            jac_cell(a, b, c, __ldg(q - 1), __ldg(q + 1), __ldg(q - nip), __ldg(q + nip), d, u);
+        d = c;
+        c = u;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// temporally blocked launch
+
+template <class C>
+static int launch_tb(const double* src, double* dst, int ni, int nj, int nk, int kfirst, int klast,
+                     double a, double b, cudaStream_t st) {
+    int* counters;
+    int sms;
+    int rc = get_counters(&counters, &sms);
+    if (rc) return rc;
+    static int occ = -1;  // per template instantiation (same device type assumed)
+    auto kern = jacobi_tb_kernel<C>;
+    if (occ < 0) {
+        cudaError_t e =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        int o = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::NT, C::SMEM_BYTES);
+        if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
+        if (o < 1) return fail(SB_ERR_CUDA, "jacobi T=%d kernel does not fit on an SM", C::T);
+        occ = o;
+    }
+    CUtensorMap smap, dmap;
+    const int64_t nip = ni + 2, njp = nj + 2, nkp = nk + 2;
+    if ((rc = make_grid_map(&smap, src, nip, njp, nkp, C::BW, C::BH))) return rc;
+    if ((rc = make_grid_map(&dmap, dst, nip, njp, nkp, C::TI, C::TJ))) return rc;
+
+    JacobiParams p;
+    p.ni = ni;
+    p.nj = nj;
+    p.nk = nk;
+    p.tiles_i = (ni + C::TI - 1) / C::TI;
+    p.tiles_j = (nj + C::TJ - 1) / C::TJ;
+    const int grid = sms * occ;
+    const int tiles = p.tiles_i * p.tiles_j;
+    // k-block: aim for ~8 items per CTA, but never shorter than 8T planes
+    // (each item re-reads 2T halo planes)
+    int want_items = grid * 8;
+    const int nkout = klast - kfirst;
+    int kb = (int)(((int64_t)tiles * nkout + want_items - 1) / want_items);
+    kb = max(kb, 8 * C::T);
+    kb = min(kb, nkout);
+    p.kfirst = kfirst;
+    p.klast = klast;
+    p.kblk = kb;
+    p.kblocks = (nkout + kb - 1) / kb;
+    p.items = tiles * p.kblocks;
+    p.a = a;
+    p.b = b;
+    p.counter = counters;
+    cudaError_t e = cudaMemsetAsync(counters, 0, sizeof(int), st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counter)");
+    const int nctas = min(grid, p.items);
+    kern<<<nctas, C::NT, C::SMEM_BYTES, st>>>(smap, dmap, p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "jacobi_tb launch");
+    return SB_OK;
+}
+
+// tile configurations per depth: <T, TI, TJ, RJ, S, MINB>
+using Cfg1 = JacobiCfg<1, 64, 16, 2, 4, 3>;
+using Cfg2 = JacobiCfg<2, 64, 16, 2, 4, 2>;
+using Cfg3 = JacobiCfg<3, 64, 8, 2, 3, 2>;
+using Cfg4 = JacobiCfg<4, 64, 8, 2, 3, 2>;
+using Cfg5 = JacobiCfg<5, 32, 8, 2, 3, 1>;
+using Cfg6 = JacobiCfg<6, 32, 8, 2, 3, 1>;
+using Cfg7 = JacobiCfg<7, 32, 8, 2, 3, 1>;
+using Cfg8 = JacobiCfg<8, 32, 8, 2, 3, 1>;
+
+static int launch_depth(int T, const double* src, double* dst, int ni, int nj, int nk, int kfirst,
+                        int klast, double a, double b, cudaStream_t st) {
+    if (klast <= kfirst) return SB_OK;
+    switch (T) {
+        case 1: return launch_tb<Cfg1>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+        case 2: return launch_tb<Cfg2>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+        case 3: return launch_tb<Cfg3>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+        case 4: return launch_tb<Cfg4>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+        case 5: return launch_tb<Cfg5>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+        case 6: return launch_tb<Cfg6>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+        case 7: return launch_tb<Cfg7>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+        case 8: return launch_tb<Cfg8>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+    }
+    return fail(SB_ERR_PLAN, "unsupported depth %d", T);
+}
+
+static int launch_generic(const double* src, double* dst, int ni, int nj, int kfirst, int klast,
+                          double a, double b, cudaStream_t st) {
+    if (klast <= kfirst) return SB_OK;
+    dim3 blk(32, 8);
+    const int kchunk = 64;
+    dim3 grd((ni + 31) / 32, (nj + 7) / 8, (klast - kfirst + kchunk - 1) / kchunk);
+    jacobi_generic_kernel<<<grd, blk, 0, st>>>(src, dst, ni, nj, kfirst, klast, kchunk, a, b);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SB_OK : cuda_fail(e, "jacobi_generic launch");
+}
+
+int check_dims(int64_t ni, int64_t nj, int64_t nk) {
+    if (ni < 1 || nj < 1 || nk < 1)
+        return fail(SB_ERR_DIMENSION, "extents must be positive, got %lldx%lldx%lld",
+                    (long long)ni, (long long)nj, (long long)nk);
+    // int32 indexing inside kernels and TMA coordinates
+    if (ni > (1 << 20) || nj > (1 << 20) || nk > (1 << 20) ||
+        (ni + 2) * (nj + 2) * (nk + 2) > (int64_t(1) << 40))
+        return fail(SB_ERR_DIMENSION, "grid %lldx%lldx%lld too large", (long long)ni,
+                    (long long)nj, (long long)nk);
+    return SB_OK;
+}
+
+bool tma_ok(const void* p, int64_t ni) {
+    return ((ni + 2) % 2 == 0) && ((reinterpret_cast<uintptr_t>(p) & 15) == 0);
+}
+
+int halo_copy(const double* src, double* dst, int ni, int nj, int nk, cudaStream_t st) {
+    halo_copy_kernel<<<256, 256, 0, st>>>(src, dst, ni, nj, nk);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SB_OK : cuda_fail(e, "halo_copy launch");
+}
+
+// T fused sweeps src -> dst (T = 1 for grids TMA cannot describe), output
+// planes [kfirst, klast) only.
+int jacobi_block(const double* src, double* dst, int ni, int nj, int nk, int kfirst, int klast,
+                 int T, double a, double b, cudaStream_t st) {
+    if (tma_ok(src, ni) && tma_ok(dst, ni))
+        return launch_depth(T, src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+    if (T != 1) return fail(SB_ERR_PLAN, "depth %d needs an even ni (16-byte row pitch)", T);
+    return launch_generic(src, dst, ni, nj, kfirst, klast, a, b, st);
+}
+
+// Advance `iters` Jacobi sweeps between two device buffers whose halos are
+// already equal.  Returns through *in_b whether the result is in `b_buf`.
+int jacobi_run(double* a_buf, double* b_buf, int ni, int nj, int nk, int64_t iters, double a,
+               double b, int depth, cudaStream_t st, int* in_b) {
+    const bool tma = tma_ok(a_buf, ni) && tma_ok(b_buf, ni);
+    double* src = a_buf;
+    double* dst = b_buf;
+    int64_t left = iters;
+    while (left > 0) {
+        int T = (int)((left >= depth) ? depth : left);
+        if (!tma) T = 1;
+        int rc = jacobi_block(src, dst, ni, nj, nk, 1, nk + 1, T, a, b, st);
+        if (rc) return rc;
+        left -= T;
+        double* t = src;
+        src = dst;
+        dst = t;
+    }
+    *in_b = (src == b_buf);
+    return SB_OK;
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+int sb_version(void) { return 100; }
+
+const char* sb_last_error(void) { return sb::last_error(); }
+
+int sb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int sb_max_depth(void) { return 8; }
+
+int sb_jacobi(double* grid, double* scratch, int64_t ni, int64_t nj, int64_t nk, int64_t iters,
+              double a, double b, int depth, void* stream, int* result_in_scratch) {
+    clear_error();
+    int rc = check_dims(ni, nj, nk);
+    if (rc) return rc;
+    if (iters < 0) return fail(SB_ERR_PLAN, "iter_end must be >= 0, got %lld", (long long)iters);
+    if (depth < 1 || depth > sb_max_depth())
+        return fail(SB_ERR_PLAN, "depth must be in [1, %d], got %d", sb_max_depth(), depth);
+    if (!grid || !scratch || !result_in_scratch) return fail(SB_ERR_ARGUMENT, "null pointer");
+    if (grid == scratch) return fail(SB_ERR_ARGUMENT, "grid and scratch must be distinct");
+    if ((reinterpret_cast<uintptr_t>(grid) | reinterpret_cast<uintptr_t>(scratch)) & 7)
+        return fail(SB_ERR_ARGUMENT, "grid buffers must be 8-byte aligned");
+    *result_in_scratch = 0;
+    if (iters == 0) return SB_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if ((rc = halo_copy(grid, scratch, (int)ni, (int)nj, (int)nk, st))) return rc;
+    return jacobi_run(grid, scratch, (int)ni, (int)nj, (int)nk, iters, a, b, depth, st,
+                      result_in_scratch);
+}
+
+double* sb_host_alloc(int64_t count) {
+    clear_error();
+    void* p = nullptr;
+    if (count <= 0) return nullptr;
+    cudaError_t e = cudaMallocHost(&p, (size_t)count * sizeof(double));
+    if (e != cudaSuccess) {
+        cuda_fail(e, "cudaMallocHost");
+        return nullptr;
+    }
+    return static_cast<double*>(p);
+}
+
+void sb_host_free(double* p) {
+    if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

@@ -1,0 +1,22 @@
+// sb_internal.h -- declarations shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace sb {
+
+int fail(int code, const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+void clear_error();
+const char* last_error();
+
+int check_dims(int64_t ni, int64_t nj, int64_t nk);
+int get_counters(int** counters, int* sms);
+bool tma_ok(const void* p, int64_t ni);
+int halo_copy(const double* src, double* dst, int ni, int nj, int nk, cudaStream_t st);
+int jacobi_run(double* a_buf, double* b_buf, int ni, int nj, int nk, int64_t iters, double a,
+               double b, int depth, cudaStream_t st, int* in_b);
+int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,
+           cudaStream_t st);
+
+}  // namespace sb

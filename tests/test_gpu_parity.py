@@ -1,0 +1,144 @@
+"""GPU parity: the B200 kernels (through the drop-in API and the C ABI)
+against the reference's own results (tests/golden, produced by the
+reference package) and against the CPU oracle.  Bitwise throughout."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import coeffs_of, make_input, sha
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (run under gpurun)")
+
+
+from paper_1004_1741_b200 import _lib  # noqa: E402
+from paper_1004_1741_b200.grid import Grid3D  # noqa: E402
+from paper_1004_1741_b200.kernels import StencilCoeffs  # noqa: E402
+from paper_1004_1741_b200.sweeps import SweepPlan, WavefrontConfig, execute, run  # noqa: E402
+
+
+def run_device(kernel, data, iters, a, b, depth):
+    g = Grid3D(data.shape[2] - 2, data.shape[1] - 2, data.shape[0] - 2,
+               torch.from_numpy(np.array(data)).cuda())
+    execute(kernel, g, iters, a, b, depth)
+    return g.data.cpu().numpy()
+
+
+def test_small_cases_host_path(small_cases):
+    """numpy grids through run(): sb_run_host (H2D, sweeps, D2H)."""
+    for name, (rec, want) in small_cases.items():
+        a, b = coeffs_of(rec)
+        g = make_input(rec["spec"])
+        out = run(SweepPlan(rec["kernel"], "serial", rec["iters"], coeffs=StencilCoeffs(a, b)), g)
+        assert sha(out.data) == sha(want), name
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3, 4, 5, 8])
+def test_small_cases_device_path_every_depth(small_cases, depth):
+    for name, (rec, want) in small_cases.items():
+        a, b = coeffs_of(rec)
+        got = run_device(rec["kernel"], make_input(rec["spec"]).data, rec["iters"], a, b, depth)
+        assert sha(got) == sha(want), (name, depth)
+
+
+def test_hashed_cases(hashed_cases):
+    for name, rec in hashed_cases.items():
+        if np.prod(rec["spec"]["shape"]) > 130 ** 3:
+            continue
+        a, b = coeffs_of(rec)
+        for depth in (1, 4):
+            got = run_device(rec["kernel"], make_input(rec["spec"]).data, rec["iters"], a, b, depth)
+            assert sha(got) == rec["output_sha256"], (name, depth)
+
+
+@pytest.mark.parametrize("key,depths", [
+    ("cfg3_jacobi512_halo1_it100", (1, 2, 4, 8)),
+    ("cfg3_jacobi512_halo1_it4", (4,)),
+    ("cfg5_gsn512_mixed_it100", (1,)),
+    ("cfg5_gsi512_mixed_it100", (1,)),
+])
+def test_baseline_configs_full_size(hashed_cases, key, depths):
+    """BASELINE configs 3 and 5 at full size (512^3 x 100) vs the reference's hash."""
+    rec = hashed_cases[key]
+    a, b = coeffs_of(rec)
+    data = make_input(rec["spec"]).data
+    for depth in depths:
+        got = run_device(rec["kernel"], data, rec["iters"], a, b, depth)
+        assert sha(got) == rec["output_sha256"], (key, depth)
+
+
+def test_random_shapes_vs_oracle():
+    rng = np.random.default_rng(7)
+    for trial in range(24):
+        ni = int(rng.integers(1, 70)) * (1 if trial % 3 else 2)
+        nj, nk = (int(x) for x in rng.integers(1, 40, size=2))
+        kernel = ("jacobi", "gs-naive", "gs-interleaved")[trial % 3]
+        iters = int(rng.integers(1, 7))
+        a, b = (0.5, 0.1) if kernel == "jacobi" else (0.0, 1 / 6)
+        data = make_input({"shape": [ni, nj, nk], "pattern": "random", "seed": trial,
+                           "lo": -1.0, "hi": 1.0}).data
+        want = oracle.run_serial(kernel, data, iters, a, b)
+        for depth in ((1, 3, 8) if kernel == "jacobi" else (1,)):
+            got = run_device(kernel, data, iters, a, b, depth)
+            assert sha(got) == sha(want), (ni, nj, nk, kernel, iters, depth)
+
+
+def test_wavefront_plan_depth_and_results(small_cases):
+    rec, want = small_cases["wf18_jacobi"]
+    a, b = coeffs_of(rec)
+    for t in (2, 4, 8):
+        g = make_input(rec["spec"]).to_device()
+        stats = {}
+        run(SweepPlan("jacobi", "wavefront", rec["iters"], coeffs=StencilCoeffs(a, b),
+                      config=WavefrontConfig(1, t, 2)), g, stats=stats)
+        assert stats["depth"] == t and stats["line_updates"] == rec["iters"] * 18 * 18
+        assert sha(g.data.cpu().numpy()) == sha(want)
+
+
+def test_halo_never_written_device():
+    g = make_input({"shape": [30, 22, 18], "pattern": "random", "seed": 3, "lo": 0.0, "hi": 1.0})
+    g.data[0] = 2.0
+    g.data[:, :, -1] = -3.0
+    before = g.data.copy()
+    mask = np.ones_like(before, dtype=bool)
+    mask[1:-1, 1:-1, 1:-1] = False
+    for kernel in ("jacobi", "gs-naive", "gs-interleaved"):
+        got = run_device(kernel, before, 5, 0.0, 1 / 6, 4)
+        assert np.array_equal(got[mask], before[mask]), kernel
+
+
+def test_c_abi_device_pointers_direct():
+    """sb_jacobi / sb_gs called through ctypes with raw device pointers."""
+    lib = _lib.load()
+    data = make_input({"shape": [64, 40, 24], "pattern": "random", "seed": 11, "lo": 0.0,
+                       "hi": 1.0}).data
+    want = oracle.run_serial("jacobi", data, 9, 0.0, 1 / 6)
+    g = torch.from_numpy(data.copy()).cuda()
+    s = torch.empty_like(g)
+    in_s = ctypes.c_int(-1)
+    _lib.check(lib.sb_jacobi(g.data_ptr(), s.data_ptr(), 64, 40, 24, 9, 0.0, 1 / 6, 4, None,
+                             ctypes.byref(in_s)))
+    _lib.check(lib.sb_sync(None))
+    got = (s if in_s.value else g).cpu().numpy()
+    assert in_s.value in (0, 1) and sha(got) == sha(want)
+    want = oracle.run_serial("gs-interleaved", data, 3, 0.0, 1 / 6)
+    g = torch.from_numpy(data.copy()).cuda()
+    _lib.check(lib.sb_gs(g.data_ptr(), 64, 40, 24, 3, 1 / 6, 2, None))
+    _lib.check(lib.sb_sync(None))
+    assert sha(g.cpu().numpy()) == sha(want)
+
+
+def test_device_errors_are_loud():
+    lib = _lib.load()
+    with pytest.raises(ValueError):
+        _lib.check(lib.sb_run_host(0, 0, 4, 4, 4, 1, 0.0, 0.1, 1, 0))
