@@ -1,0 +1,416 @@
+"""Benchmark: BASELINE.json metric "MLUP/s (fp64) 3D 7-pt Jacobi & lexicographic
+GS; % of HBM roofline; 1/2/4/8 GPU".
+
+Headline workload (config.workload): BASELINE config 4, weak scaling --
+Jacobi on a 1024 x 1024 x (1024 * N) interior, 1024^3 per GPU, z-slabs with
+per-time-block halo exchange, 100 sweeps per step, temporal depth --depth.
+At N=1 this is the largest single-GPU configuration of BASELINE.json.
+A step = 100 sweeps over the resident grid (13.4 / 107.4 GLUP per GPU for
+512^3 / 1024^3); MLUP/s = sweeps * cells / time (reference perf.py:262).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--depth T]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference     # the reference's CPU path (oracle port)
+
+Printed: ONE JSON line on rank 0.  Side measurements at N=1 (config 3's
+depth sweep at 512^3, config 5's Gauss-Seidel) go under "also".
+"""
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS = {"hbm_gbs": 6534.5, "source": "fallback"}
+try:
+    _mp = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    PEAKS = {"hbm_gbs": float(_mp["hbm_gbs"]), "source": "measured"}
+except Exception:  # noqa: BLE001
+    PEAKS = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+METRIC = "MLUP/s (fp64) 3D 7-pt Jacobi & lexicographic GS; % of HBM roofline; 1/2/4/8 GPU"
+SWEEPS = 100
+NI = NJ = NK_PER_GPU = 1024
+
+
+# ----------------------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[4:8]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def synth_slab(torch, eng, dev):
+    """Deterministic synthetic field over global plane index (consistent
+    across ranks, so ghosts equal the neighbours' owned planes): values in
+    [0, 1), zero Dirichlet halo -- the shape/value distribution of config 4."""
+    nkl2 = eng.nkl + 2
+    k = torch.arange(eng.k0, eng.k0 + nkl2, device=dev, dtype=torch.float64)[:, None, None]
+    j = torch.arange(NJ + 2, device=dev, dtype=torch.float64)[None, :, None]
+    i = torch.arange(NI + 2, device=dev, dtype=torch.float64)[None, None, :]
+    x = torch.frac(torch.sin(k * 12.9898 + j * 78.233 + i * 37.719) * 43758.5453).abs()
+    x[:, 0], x[:, -1], x[:, :, 0], x[:, :, -1] = 0.0, 0.0, 0.0, 0.0
+    nk_total = NK_PER_GPU * eng.world
+    if eng.k0 == 0:
+        x[0] = 0.0
+    if eng.k0 + nkl2 - 1 == nk_total + 1:
+        x[-1] = 0.0
+    return x
+
+
+def cpu_reference_rate(budget_s=12.0, n=512, threads=None):
+    """The reference's CPU path (oracle port of the threaded k-slab Jacobi
+    engine, reference sweeps/threaded.py:28-59) on the host cores: a bounded
+    sample of the workload (n^3 interior, S sweeps sized to ~budget_s)."""
+    import numpy as np
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle  # CPU baseline only
+
+    threads = threads or os.cpu_count() or 1
+    g = np.random.default_rng(42).random((n + 2, n + 2, n + 2))
+    g[0], g[-1], g[:, 0], g[:, -1], g[:, :, 0], g[:, :, -1] = 0, 0, 0, 0, 0, 0
+    t0 = time.perf_counter()
+    oracle.run_threaded("jacobi", g, 2, 0.0, 1 / 6, threads=threads)
+    calib = (time.perf_counter() - t0) / 2
+    sweeps = int(max(2, min(200, budget_s / max(calib, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.run_threaded("jacobi", g, sweeps, 0.0, 1 / 6, threads=threads)
+    sec = time.perf_counter() - t0
+    return {"value": sweeps * n ** 3 / sec / 1e6, "unit": "MLUP/s", "cores": threads,
+            "kind": "port",
+            "sample": f"{n}^3 interior, {sweeps} Jacobi sweeps, oracle port of the reference's "
+                      f"threaded k-slab engine on {threads} host threads"}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    n = 512
+    rates, secs = [], []
+    budget = max(5.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for step in range(args.warmup + args.steps):
+        r = cpu_reference_rate(budget_s=budget, n=n)
+        if step >= args.warmup:
+            rates.append(r["value"])
+            secs.append(budget)
+    value = statistics.median(rates)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "MLUP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg4-weak Jacobi (bounded CPU sample: 512^3 x S sweeps per step)",
+                       "sample_n": n, "parallelism": f"{os.cpu_count()} host threads"},
+            "cpu_baseline": dict(r, value=value),
+            "e2e": {"value": value, "unit": "MLUP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def time_gs(torch, lib, n, iters, kid, reps=2):
+    from paper_1004_1741_b200 import _lib
+
+    g = torch.rand((n + 2, n + 2, n + 2), dtype=torch.float64, device="cuda") * 2 - 1
+    g[0], g[-1], g[:, 0], g[:, -1], g[:, :, 0], g[:, :, -1] = 0, 0, 0, 0, 0, 0
+    st = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(st.cuda_stream)
+    _lib.check(lib.sb_gs(g.data_ptr(), n, n, n, 2, 1 / 6, kid, sp))
+    _lib.check(lib.sb_sync(sp))
+    best = None
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        _lib.check(lib.sb_gs(g.data_ptr(), n, n, n, iters, 1 / 6, kid, sp))
+        e1.record(st)
+        _lib.check(lib.sb_sync(sp))
+        s = e0.elapsed_time(e1) / 1e3
+        best = s if best is None else min(best, s)
+    mlups = iters * n ** 3 / best / 1e6
+    return {"mlups": mlups, "roofline_frac": mlups * 1e6 * 16 / (PEAKS["hbm_gbs"] * 1e9),
+            "ms": best * 1e3, "sweeps": iters, "n": n}
+
+
+def time_jacobi_depths(torch, lib, n, iters, depths):
+    from paper_1004_1741_b200 import _lib
+
+    g = torch.rand((n + 2, n + 2, n + 2), dtype=torch.float64, device="cuda")
+    g[0], g[-1], g[:, 0], g[:, -1], g[:, :, 0], g[:, :, -1] = 1, 1, 1, 1, 1, 1
+    s = torch.empty_like(g)
+    st = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(st.cuda_stream)
+    out = {}
+    for d in depths:
+        r = ctypes.c_int(0)
+        _lib.check(lib.sb_jacobi(g.data_ptr(), s.data_ptr(), n, n, n, d, 0.0, 1 / 6, d, sp,
+                                 ctypes.byref(r)))
+        best = None
+        for _ in range(2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            _lib.check(lib.sb_jacobi(g.data_ptr(), s.data_ptr(), n, n, n, iters, 0.0, 1 / 6, d, sp,
+                                     ctypes.byref(r)))
+            e1.record(st)
+            _lib.check(lib.sb_sync(sp))
+            sec = e0.elapsed_time(e1) / 1e3
+            best = sec if best is None else min(best, sec)
+        mlups = iters * n ** 3 / best / 1e6
+        out[f"T{d}"] = {"mlups": mlups, "ms": best * 1e3,
+                        "x_single_sweep_roofline": mlups * 1e6 * 16 / (PEAKS["hbm_gbs"] * 1e9)}
+    return out
+
+
+def run_gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1004_1741_b200 import _lib
+    from paper_1004_1741_b200.slabs import SlabEngine, gpu_compute
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+    depth = args.depth
+    nk_total = NK_PER_GPU * world
+    eng = SlabEngine(NI, NJ, nk_total, depth, rank, world, gpu_compute(NI, NJ, 0.0, 1.0 / 6.0),
+                     like=torch.empty(0, dtype=torch.float64, device=dev))
+    x = synth_slab(torch, eng, dev)
+    eng.bufs[0].copy_(x)
+    eng.bufs[1].copy_(x)
+    del x
+    st = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    # launch-level events on the compute stream (roofline): per period, the
+    # interior launch is bracketed; at N=1 that is the whole fused block.
+    period_events = []
+
+    def step(record):
+        left = SWEEPS
+        while left > 0:
+            t = min(depth, left)
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+            eng.period(t)
+            if record:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(st)
+                period_events.append((t, e0, e1))
+            left -= t
+        eng.wait()
+
+    for _ in range(args.warmup):
+        step(False)
+    barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t_start.record(st)
+        for _ in range(args.steps):
+            step(True)
+        t_end.record(st)
+        barrier()
+    sec = t_start.elapsed_time(t_end) / 1e3
+    if world > 1:
+        tt = torch.tensor([sec], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        sec = float(tt.item())
+    cells_per_gpu = NI * NJ * NK_PER_GPU
+    lups = SWEEPS * cells_per_gpu * world * args.steps
+    value = lups / sec / 1e6
+    launches = args.steps * sum(1 if world == 1 else 3 for _ in range(-(-SWEEPS // depth)))
+
+    # roofline of the dominant kernel (the fused T-sweep Jacobi launch):
+    # algorithmic bytes per launch = 16 B (one read + one write) per owned cell
+    full = [(t, e0.elapsed_time(e1) / 1e3) for t, e0, e1 in period_events if t == depth]
+    avg = sum(s for _, s in full) / max(1, len(full))
+    algo_bytes = 16.0 * cells_per_gpu
+    achieved = algo_bytes / avg / 1e9 if avg > 0 else None
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get(f"jacobi_tb_T{depth}_1024")
+        except Exception:  # noqa: BLE001
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": PEAKS["hbm_gbs"], "unit": "GB/s",
+                "frac": (achieved / PEAKS["hbm_gbs"]) if achieved else None, "traffic": traffic,
+                "peak_source": PEAKS["source"], "kernel": f"jacobi_tb_kernel<T={depth}>",
+                "algorithmic_bytes_per_launch": algo_bytes, "avg_launch_ms": avg * 1e3,
+                "sweeps_per_launch": depth,
+                "single_sweep_roofline_mlups": PEAKS["hbm_gbs"] * 1e9 / 16 / 1e6,
+                "x_single_sweep_roofline": value / world / (PEAKS["hbm_gbs"] * 1e9 / 16 / 1e6)}
+
+    # e2e through the public C-ABI host-buffer entry point (sb_run_host):
+    # pinned host grid -> H2D -> sweeps -> D2H, every step
+    e2e = None
+    if not args.no_e2e:
+        host = _lib.pinned_array(tuple(eng.bufs[0].shape))
+        host[...] = eng.bufs[eng.cur].cpu().numpy() if world == 1 else 0.0
+        if world == 1:
+            nbytes = host.nbytes
+            _lib.check(lib.sb_run_host(0, host.ctypes.data, NI, NJ, NK_PER_GPU, depth, 0.0, 1 / 6,
+                                       depth, local))  # warm
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                _lib.check(lib.sb_run_host(0, host.ctypes.data, NI, NJ, NK_PER_GPU, SWEEPS, 0.0,
+                                           1 / 6, depth, local))
+            esec = time.perf_counter() - t0
+            e2e = {"value": SWEEPS * cells_per_gpu * args.steps / esec / 1e6, "unit": "MLUP/s",
+                   "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                   "path": "sb_run_host (C ABI, pinned host grid, copies inside the timed region)"}
+        else:
+            e2e = run_e2e_multi(torch, dist, eng, host, args, dev, st, world)
+        del host
+
+    also = {}
+    if world == 1 and not args.no_also:
+        n5 = 512
+        also["cfg3_jacobi512_depths"] = time_jacobi_depths(torch, lib, n5, 96, [1, 2, 4, 8])
+        also["cfg5_gs512_naive"] = time_gs(torch, lib, n5, args.gs_sweeps, 1)
+        also["cfg5_gs512_interleaved"] = time_gs(torch, lib, n5, args.gs_sweeps, 2)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_reference_rate(budget_s=args.cpu_budget)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "MLUP/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec / args.steps * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (deterministic sin-hash field in [0,1), zero Dirichlet halo)",
+                "config": {"workload": "BASELINE cfg4 weak: Jacobi 1024x1024x(1024*N), "
+                                       "100 sweeps/step, z-slabs + halo exchange",
+                           "ni": NI, "nj": NJ, "nk": nk_total, "sweeps_per_step": SWEEPS,
+                           "depth": depth, "coeffs": [0.0, 1 / 6],
+                           "parallelism": f"z-slabs x{world}" if world > 1 else "1 GPU",
+                           "l2": "inputs larger than L2 (8.6 GB/GPU per buffer)"},
+                "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "clocks": clk.summary(), "also": also}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e_multi(torch, dist, eng, host, args, dev, st, world):
+    """Per rank: host slab -> H2D -> the same slab engine -> D2H, timed as
+    the max over ranks."""
+    nbytes = host.nbytes
+    src = torch.from_numpy(host)
+    dist.barrier(device_ids=[dev.index])
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        eng.bufs[0].copy_(src, non_blocking=True)
+        eng.bufs[1].copy_(eng.bufs[0])
+        eng.cur = 0
+        eng.run(SWEEPS)
+        src.copy_(eng.field, non_blocking=True)
+        torch.cuda.synchronize()
+    esec = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+    dist.all_reduce(esec, op=dist.ReduceOp.MAX)
+    return {"value": SWEEPS * NI * NJ * NK_PER_GPU * world * args.steps / float(esec.item()) / 1e6,
+            "unit": "MLUP/s", "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
+            "path": "per-rank pinned host slab, H2D + slab engine + D2H"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--depth", type=int, default=4)
+    ap.add_argument("--gs-sweeps", type=int, default=20)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-also", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl != "reference":
+        print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

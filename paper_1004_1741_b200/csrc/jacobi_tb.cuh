@@ -10,8 +10,9 @@
 // loads) and only the last writes it (TMA plane stores), so HBM traffic is
 // 16/T bytes per lattice-site update.
 //
-// Tiling: an output tile is TI x TJ cells of an xy plane, over a range of
-// z-planes [kb, ke).  The input box of a plane is (TI+2H) x (TJ+2T) with
+// Tiling: an output tile is (TI+2) x TJ cells of an xy plane (tiles start
+// every TI columns at even i; see JacobiCfg::TO), over a range of z-planes
+// [kb, ke).  The input box of a plane is (TI+2+2H) x (TJ+2T) with
 // H = T rounded up to even (overlapped/trapezoid halo: level L is valid on
 // the box shrunk by L cells, so level T is valid on the output tile).  Each
 // thread owns a 2(i) x RJ(j) block of cells at every level, keeps each
@@ -55,18 +56,23 @@ struct JacobiParams {
 template <int T_, int TI_, int TJ_, int RJ_, int S_, int MINB_>
 struct JacobiCfg {
     static constexpr int T = T_, TI = TI_, TJ = TJ_, RJ = RJ_, S = S_, MINB = MINB_;
+    // Along i every TMA box must start on an even index (16-byte aligned
+    // fp64 rows), so tiles start at even padded i (stride TI) and write
+    // TO = TI + 2 columns; neighbouring tiles overlap by two columns and
+    // write bitwise-identical values there.
+    static constexpr int TO = TI + 2;                  // output columns per tile
     static constexpr int H = (T + 1) / 2 * 2;          // input halo along i (even)
     static constexpr int HP = (T - 1 + 1) / 2 * 2;     // computed halo along i at level 1 (even)
-    static constexpr int BW = TI + 2 * H;              // input box width
+    static constexpr int BW = TO + 2 * H;              // input box width
     static constexpr int BH = TJ + 2 * T;              // input box rows
     static constexpr int PLANE = BW * BH;              // doubles per plane buffer
     static constexpr int PSTRIDE = (PLANE + 15) / 16 * 16;  // 128-B aligned (TMA destination)
-    static constexpr int TC = TI / 2 + HP;             // thread columns (cell pairs)
+    static constexpr int TC = TO / 2 + HP;             // thread columns (cell pairs)
     static constexpr int ROWS1 = TJ + 2 * (T - 1);     // rows computed at level 1
     static_assert(ROWS1 % RJ == 0, "rows per thread must divide the level-1 row count");
     static constexpr int TR = ROWS1 / RJ;              // thread rows
     static constexpr int NT = TC * TR;                 // threads per CTA
-    static constexpr int OUT = TI * TJ;                // doubles per output tile
+    static constexpr int OUT = TO * TJ;                // doubles per output tile
     static constexpr int NLVL = (T > 1) ? (T - 1) : 0; // smem level planes (levels 1..T-1)
     static constexpr int QSLOTS = 4;                   // item queue depth
     // smem layout (in doubles): ring[S] | lvl[NLVL][2] | out[2] ; then barriers + item queue
@@ -79,7 +85,7 @@ struct JacobiCfg {
 };
 
 struct ItemInfo {
-    int I0, J0;    // output tile origin (padded coordinates)
+    int I0, J0;    // output tile origin (padded coordinates; I0 even)
     int kb, N;     // first output plane, number of plane steps (ke - kb + 2T); N == 0: stop
 };
 
@@ -104,7 +110,7 @@ __device__ __forceinline__ ItemInfo decode_item(const JacobiParams& p, int item)
     const int kbi = item / per_block;
     const int t = item - kbi * per_block;
     const int ti = t % p.tiles_i, tj = t / p.tiles_i;
-    it.I0 = 1 + C::TI * ti;
+    it.I0 = C::TI * ti;
     it.J0 = 1 + C::TJ * tj;
     it.kb = p.kfirst + kbi * p.kblk;
     const int ke = min(it.kb + p.kblk, p.klast);
@@ -208,7 +214,7 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
             const bool kin = (kL >= 1) && (kL <= p.nk);
             // region of level L actually needed downstream: tile +- (T-L)
             const int need = T - L;
-            const bool act = (di + 1 >= -need) && (di < TI + need) && (dj + RJ - 1 >= -need) &&
+            const bool act = (di + 1 >= -need) && (di < C::TO + need) && (dj + RJ - 1 >= -need) &&
                              (dj < TJ + need);
             const double* src = (L == 1) ? prv : (lvl + size_t((L - 2) * 2 + ((consumed + 1) & 1)) * PSTRIDE);
             double nv[RJ][2];
@@ -243,12 +249,12 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
             } else if (n >= 2 * T) {
                 // output tile cells: i - I0 in [0, TI), j - J0 in [0, TJ)
                 double* ob = outb + size_t(consumed & 1) * ((C::OUT + 15) / 16 * 16);
-                if (di >= 0 && di < TI) {
+                if (di >= 0 && di < C::TO) {
 #pragma unroll
                     for (int r = 0; r < RJ; ++r) {
                         const int jj = dj + r;
                         if (jj >= 0 && jj < TJ)
-                            *reinterpret_cast<double2*>(ob + jj * TI + di) =
+                            *reinterpret_cast<double2*>(ob + jj * C::TO + di) =
                                 make_double2(nv[r][0], nv[r][1]);
                     }
                 }

@@ -10,6 +10,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -200,7 +201,7 @@ static int launch_tb(const double* src, double* dst, int ni, int nj, int nk, int
     CUtensorMap smap, dmap;
     const int64_t nip = ni + 2, njp = nj + 2, nkp = nk + 2;
     if ((rc = make_grid_map(&smap, src, nip, njp, nkp, C::BW, C::BH))) return rc;
-    if ((rc = make_grid_map(&dmap, dst, nip, njp, nkp, C::TI, C::TJ))) return rc;
+    if ((rc = make_grid_map(&dmap, dst, nip, njp, nkp, C::TO, C::TJ))) return rc;
 
     JacobiParams p;
     p.ni = ni;

@@ -43,12 +43,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     return ok != 0;
 }
 // Bounded wait: a TMA transfer that never lands (a bug) traps the kernel
-// after ~2^36 cycles (tens of seconds) instead of hanging the GPU.
+// after ~2^32 cycles (about two seconds) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
     const long long t0 = clock64();
     while (!mbar_try_wait(bar, parity)) {
-        if (clock64() - t0 > (1LL << 36)) __trap();
+        if (clock64() - t0 > (1LL << 32)) __trap();
     }
 }
 

@@ -1,0 +1,144 @@
+"""Multi-GPU Jacobi: z-slabs with per-time-block halo exchange.
+
+The multi-GPU form of the reference's k-slab threading
+(sweeps/threaded.py:28-59: ``partition_blocks(nk, P)`` contiguous k-ranges,
+one barrier per sweep).  One process per GPU (torchrun); rank r owns the
+interior planes ``partition_blocks(nk, world)[r]`` and stores ``depth``
+ghost planes toward each neighbour (``slab_layout``; identical to the C
+ABI's ``sb_slab_layout``).  A period advances ``T <= depth`` sweeps:
+
+1. compute the owned planes the neighbours need (``depth`` at each inner
+   edge) -- ``sb_jacobi_planes`` restricted to those planes;
+2. post the halo exchange (NCCL send/recv of contiguous planes over
+   NVLink; on the CPU test path gloo) -- it waits only for step 1;
+3. compute the remaining owned planes while the exchange is in flight;
+4. wait for the exchange before the next period reads the ghosts.
+
+Each owned plane sees exactly the values a single-grid run would (its
+dependence cone after T sweeps stays inside owned + ghost planes), so the
+result is bitwise identical to one GPU and to the reference.
+
+The compute step is injected: on GPUs it is ``gpu_compute`` (the library);
+the CPU test suite runs the same exchange logic with an oracle compute.
+"""
+
+import ctypes
+
+from . import _lib
+from .sweeps.plan import partition_blocks
+
+
+def slab_layout(nk, nslabs, slab, depth):
+    """(own_lo, own_hi, ghost_lo, ghost_hi) in global padded plane indices;
+    mirrors sb_slab_layout (host.cu) -- tests/test_lib.py pins them equal."""
+    lo, hi = partition_blocks(nk, nslabs)[slab]
+    ghost_lo = 1 if slab == 0 else depth
+    ghost_hi = 1 if slab == nslabs - 1 else depth
+    if nslabs > 1 and hi - lo < depth:
+        from .errors import PartitionError
+
+        raise PartitionError(f"slab {slab} owns {hi - lo} planes, fewer than depth {depth}")
+    return lo + 1, hi + 1, ghost_lo, ghost_hi
+
+
+def gpu_compute(ni, nj, a, b):
+    """compute(src, dst, nk_local, k_out_lo, k_out_hi, sweeps) on the current stream."""
+    import torch
+
+    lib = _lib.load()
+
+    def compute(src, dst, nkl, k_lo, k_hi, sweeps):
+        if k_hi <= k_lo:
+            return
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(lib.sb_jacobi_planes(src.data_ptr(), dst.data_ptr(), ni, nj, nkl, k_lo, k_hi,
+                                        sweeps, a, b, stream))
+
+    return compute
+
+
+class SlabEngine:
+    """This rank's slab of a z-slab decomposed Jacobi run."""
+
+    def __init__(self, ni, nj, nk, depth, rank, world, compute, like, group=None):
+        """like: a tensor whose device/dtype the slab buffers use."""
+        import torch
+
+        self.ni, self.nj, self.nk, self.depth = ni, nj, nk, depth
+        self.rank, self.world, self.group = rank, world, group
+        self.compute = compute
+        self.own_lo, self.own_hi, self.glo, self.ghi = slab_layout(nk, world, rank, depth)
+        self.n_own = self.own_hi - self.own_lo
+        self.nkl = self.n_own + self.glo + self.ghi - 2  # local interior planes
+        self.k0 = self.own_lo - self.glo                # global index of local plane 0
+        shape = (self.nkl + 2, nj + 2, ni + 2)
+        self.bufs = [torch.empty(shape, dtype=like.dtype, device=like.device),
+                     torch.empty(shape, dtype=like.dtype, device=like.device)]
+        self.cur = 0
+        self.pending = []
+
+    # -- data movement ---------------------------------------------------------------
+    @property
+    def field(self):
+        """Local buffer holding the current field (owned planes exact)."""
+        return self.bufs[self.cur]
+
+    def load_global(self, global_data):
+        """Fill both buffers from the global padded grid (host or device)."""
+        import torch
+
+        part = global_data[self.k0:self.k0 + self.nkl + 2]
+        if not torch.is_tensor(part):
+            part = torch.from_numpy(part)
+        self.bufs[0].copy_(part)
+        self.bufs[1].copy_(self.bufs[0])
+        self.cur = 0
+
+    def owned(self):
+        """View of the owned planes of the current field."""
+        return self.field[self.glo:self.glo + self.n_own]
+
+    # -- one period -----------------------------------------------------------------
+    def _exchange(self, dst):
+        import torch.distributed as dist
+
+        ops = []
+        d = self.depth
+        hi = self.glo + self.n_own
+        if self.rank + 1 < self.world:
+            ops.append(dist.P2POp(dist.isend, dst[hi - d:hi], self.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, dst[hi:hi + d], self.rank + 1, self.group))
+        if self.rank > 0:
+            ops.append(dist.P2POp(dist.isend, dst[self.glo:self.glo + d], self.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, dst[0:self.glo], self.rank - 1, self.group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def wait(self):
+        for w in self.pending:
+            w.wait()
+        self.pending = []
+
+    def period(self, sweeps):
+        """Advance `sweeps` (<= depth) sweeps; the exchange stays in flight
+        until the next period (or wait())."""
+        assert 1 <= sweeps <= self.depth
+        self.wait()
+        src, dst = self.bufs[self.cur], self.bufs[self.cur ^ 1]
+        lo, hi, d = self.glo, self.glo + self.n_own, self.depth
+        inner_lo = min(lo + d, hi) if self.rank > 0 else lo
+        inner_hi = max(hi - d, inner_lo) if self.rank + 1 < self.world else hi
+        if self.rank > 0:
+            self.compute(src, dst, self.nkl, lo, inner_lo, sweeps)
+        if self.rank + 1 < self.world:
+            self.compute(src, dst, self.nkl, inner_hi, hi, sweeps)
+        self.pending = list(self._exchange(dst)) if self.world > 1 else []
+        self.compute(src, dst, self.nkl, inner_lo, inner_hi, sweeps)
+        self.cur ^= 1
+
+    def run(self, iters):
+        left = iters
+        while left > 0:
+            t = min(self.depth, left)
+            self.period(t)
+            left -= t
+        self.wait()
