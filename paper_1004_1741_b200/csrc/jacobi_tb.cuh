@@ -6,33 +6,36 @@
 // t threads of a group each own one sweep and trail each other by two
 // planes through a j-block held in the shared cache; here, the T "levels"
 // of a CTA each own one sweep and trail each other by one plane through an
-// xy tile held in shared memory.  Only the first level reads HBM (TMA plane
-// loads) and only the last writes it (TMA plane stores), so HBM traffic is
-// 16/T bytes per lattice-site update.
+// xy tile held on chip.  Only level 1 reads HBM (TMA plane loads into a
+// shared-memory ring) and only level T writes it, so HBM traffic is 16/T
+// bytes per lattice-site update.
 //
-// Tiling: an output tile is (TI+2) x TJ cells of an xy plane (tiles start
-// every TI columns at even i; see JacobiCfg::TO), over a range of z-planes
-// [kb, ke).  The input box of a plane is (TI+2+2H) x (TJ+2T) with
-// H = T rounded up to even (overlapped/trapezoid halo: level L is valid on
-// the box shrunk by L cells, so level T is valid on the output tile).  Each
-// thread owns a 2(i) x RJ(j) block of cells at every level, keeps each
-// level's z-queue (planes k-1, k, k+1 of the level below) in registers and
-// exchanges in-plane neighbours through one double-buffered smem plane per
-// level.  One __syncthreads per plane step.
+// Data placement (chosen from ncu: the first version was shared-memory
+// bound, 82% of the LSU/smem pipe with 2-way bank conflicts):
+//   * a warp spans the whole 64-cell tile width (lane = 2 cells, i-pairs),
+//     so W/E neighbours are warp shuffles;
+//   * a thread owns RJ consecutive rows, so N/S neighbours are registers,
+//     except at warp-strip boundaries, which go through a small
+//     double-buffered shared "exchange" row per warp and level;
+//   * the z-queue (planes k-1, k, k+1 of the level below) lives in
+//     registers; levels trail by one plane, one __syncthreads per plane;
+//   * output rows leave with coalesced 16-byte global stores.
+// Overlapped (trapezoid) tiling: level L is valid on the tile grown by T-L
+// cells; rows outside that region skip their arithmetic.
 //
 // Arithmetic (reference kernels.py:125-134):
 //     v = a*c + b*(((((W+E)+S)+N)+D)+U)
-// with explicit round-to-nearest intrinsics (no FMA contraction; the
-// library is also built with -fmad=false), so results are bitwise equal to
-// the reference for every T.  Halo (Dirichlet) cells are never computed:
-// at every level they carry the input value, and the output keeps them.
+// with explicit round-to-nearest intrinsics (no contraction; the library
+// is also built with -fmad=false): bitwise equal to the reference for
+// every T.  (A specialisation for a == 0 that drops a*c and patches the
+// sign-of-zero / non-finite cases was measured slower: its integer checks
+// cost more issue slots than the two DP operations they save.)  Halo (Dirichlet) cells are never computed: at every level they carry the
+// input value.
 //
 // Work distribution: persistent CTAs grab (tile, k-block) items from a
-// global atomic counter, in k-block-major order so that CTAs working at the
-// same time hold neighbouring tiles of the same planes (their overlapping
-// halo reads hit L2).  The TMA producer runs S-1 plane steps ahead of the
-// compute, across item boundaries, so the pipeline never drains between
-// items.
+// global atomic counter in k-block-major order (CTAs running together hold
+// neighbouring tiles of the same planes, so overlapping halo reads hit L2).
+// The TMA producer runs S-1 planes ahead, across item boundaries.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -47,41 +50,35 @@ struct JacobiParams {
     int kfirst, klast;       // output planes [kfirst, klast) (padded indices, within [1, nk])
     int tiles_i, tiles_j;    // output tiles per plane
     int kblk;                // planes per work item
-    int kblocks;             // ceil(nk / kblk)
+    int kblocks;             // ceil((klast - kfirst) / kblk)
     int items;               // tiles_i * tiles_j * kblocks
     double a, b;
     int* counter;            // work counter (zeroed before launch)
+    double* dst;             // output grid
 };
 
-template <int T_, int TI_, int TJ_, int RJ_, int S_, int MINB_>
+template <int T_, int RJ_, int NW_, int S_, int MINB_>
 struct JacobiCfg {
-    static constexpr int T = T_, TI = TI_, TJ = TJ_, RJ = RJ_, S = S_, MINB = MINB_;
-    // Along i every TMA box must start on an even index (16-byte aligned
-    // fp64 rows), so tiles start at even padded i (stride TI) and write
-    // TO = TI + 2 columns; neighbouring tiles overlap by two columns and
-    // write bitwise-identical values there.
-    static constexpr int TO = TI + 2;                  // output columns per tile
-    static constexpr int H = (T + 1) / 2 * 2;          // input halo along i (even)
-    static constexpr int HP = (T - 1 + 1) / 2 * 2;     // computed halo along i at level 1 (even)
-    static constexpr int BW = TO + 2 * H;              // input box width
-    static constexpr int BH = TJ + 2 * T;              // input box rows
-    static constexpr int PLANE = BW * BH;              // doubles per plane buffer
-    static constexpr int PSTRIDE = (PLANE + 15) / 16 * 16;  // 128-B aligned (TMA destination)
-    static constexpr int TC = TO / 2 + HP;             // thread columns (cell pairs)
-    static constexpr int ROWS1 = TJ + 2 * (T - 1);     // rows computed at level 1
-    static_assert(ROWS1 % RJ == 0, "rows per thread must divide the level-1 row count");
-    static constexpr int TR = ROWS1 / RJ;              // thread rows
-    static constexpr int NT = TC * TR;                 // threads per CTA
-    static constexpr int OUT = TO * TJ;                // doubles per output tile
-    static constexpr int NLVL = (T > 1) ? (T - 1) : 0; // smem level planes (levels 1..T-1)
-    static constexpr int QSLOTS = 4;                   // item queue depth
-    // smem layout (in doubles): ring[S] | lvl[NLVL][2] | out[2] ; then barriers + item queue
-    static constexpr size_t RING_OFF = 16;             // 128-B guard before the first buffer
-    static constexpr size_t LVL_OFF = RING_OFF + size_t(S) * PSTRIDE;
-    static constexpr size_t OUT_OFF = LVL_OFF + size_t(NLVL) * 2 * PSTRIDE;
-    static constexpr size_t DBL_END = OUT_OFF + 2 * size_t((OUT + 15) / 16 * 16);
+    static constexpr int T = T_, RJ = RJ_, NW = NW_, S = S_, MINB = MINB_;
+    static constexpr int H = (T + 1) / 2 * 2;          // input halo along i (even: TMA boxes
+                                                       // must start 16-byte aligned)
+    static constexpr int BW = 64;                      // cells per warp row (32 lanes x 2)
+    static constexpr int TO = BW - 2 * H;              // output columns per tile (= i stride)
+    static constexpr int ROWS = NW * RJ;               // rows computed per tile (level-1 region)
+    static constexpr int TJ = ROWS - 2 * (T - 1);      // output rows per tile
+    static_assert(TJ >= 1, "tile too short for this depth");
+    static constexpr int BH = ROWS + 2;                // input box rows (+1 neighbour row each side)
+    static constexpr int BOX = BW * BH;
+    static constexpr int BOXS = (BOX + 15) / 16 * 16;  // 128-B aligned TMA destinations
+    static constexpr int NT = NW * 32;
+    static constexpr int XROW = 2 * BW;                // exchange doubles per warp: top + bottom row
+    static constexpr int NX = (T > 1) ? (T - 1) : 0;   // levels with exchange rows (1..T-1)
+    static constexpr int QSLOTS = 4;
+    static constexpr size_t RING_OFF = 0;
+    static constexpr size_t X_OFF = RING_OFF + size_t(S) * BOXS;
+    static constexpr size_t DBL_END = X_OFF + size_t(NX) * 2 * NW * XROW;
     static constexpr size_t SMEM_BYTES = DBL_END * 8 + 8 * S + 16 * QSLOTS + 64;
-    static constexpr uint32_t BOX_BYTES = uint32_t(BW) * BH * 8;
+    static constexpr uint32_t BOX_BYTES = uint32_t(BOX) * 8;
 };
 
 struct ItemInfo {
@@ -110,7 +107,7 @@ __device__ __forceinline__ ItemInfo decode_item(const JacobiParams& p, int item)
     const int kbi = item / per_block;
     const int t = item - kbi * per_block;
     const int ti = t % p.tiles_i, tj = t / p.tiles_i;
-    it.I0 = C::TI * ti;
+    it.I0 = C::TO * ti;
     it.J0 = 1 + C::TJ * tj;
     it.kb = p.kfirst + kbi * p.kblk;
     const int ke = min(it.kb + p.kblk, p.klast);
@@ -118,194 +115,244 @@ __device__ __forceinline__ ItemInfo decode_item(const JacobiParams& p, int item)
     return it;
 }
 
+__device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void sts2(double* p, double x, double y) {
+    *reinterpret_cast<double2*>(p) = make_double2(x, y);
+}
+
+// Per-thread state of one level's input: three plane slots rotating with
+// the step phase (D, C, U = slots PH, PH+1, PH+2 mod 3), RJ rows x 2 cells.
 template <class C>
-__global__ void __launch_bounds__(C::NT, C::MINB)
-jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
-                 const __grid_constant__ CUtensorMap dst_map, const JacobiParams p) {
-    constexpr int T = C::T, TI = C::TI, TJ = C::TJ, RJ = C::RJ, S = C::S;
-    constexpr int BW = C::BW, PSTRIDE = C::PSTRIDE;
-    extern __shared__ __align__(128) double smem[];
-    double* ring = smem + C::RING_OFF;
-    double* lvl = smem + C::LVL_OFF;
-    double* outb = smem + C::OUT_OFF;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DBL_END);
-    ItemInfo* queue = reinterpret_cast<ItemInfo*>(full + S);
+struct LevelQ {
+    double q[3][C::RJ][2];
+};
 
+// The final operation of a cell.  Reference: RN(RN(a*c) + RN(b*acc)).  When
+// a == +-0 the product a*c is exact (a signed zero, or NaN for non-finite
+// c), so RN(a*c + RN(b*acc)) -- one fused multiply-add -- is the same value
+// bit for bit, including signed zeros and NaNs; it saves one DP operation.
+template <bool AZ>
+__device__ __forceinline__ double jac_final(double a, double b, double c, double acc) {
+    if (AZ) return __fma_rn(a, c, __dmul_rn(b, acc));
+    return __dadd_rn(__dmul_rn(a, c), __dmul_rn(b, acc));
+}
+
+struct JState {      // per-CTA loop state shared by the step functions
+    uint32_t g;      // global plane-step counter (ring phase, exchange parity, rotation)
+    int n, cq;       // step within the item, consumer queue slot
+    ItemInfo it;     // current item
+    uint32_t ld_issued;
+    int pq, pn;      // producer queue slot / plane step
+    ItemInfo pitem;  // producer's item
+};
+
+template <class C>
+__device__ __forceinline__ void produce(const CUtensorMap* src_map, const JacobiParams& p,
+                                        double* ring, uint64_t* full, ItemInfo* queue, JState& s) {
+    constexpr int S = C::S;
+    uint64_t* bar = &full[s.ld_issued % S];
+    mbar_arrive_expect_tx(bar, C::BOX_BYTES);
+    tma_load_3d(ring + size_t(s.ld_issued % S) * C::BOXS, src_map, s.pitem.I0 - C::H,
+                s.pitem.J0 - C::T, s.pitem.kb - C::T + s.pn, bar);
+    ++s.ld_issued;
+    if (++s.pn == s.pitem.N) {
+        s.pn = 0;
+        s.pq = (s.pq + 1) % C::QSLOTS;
+        s.pitem = decode_item<C>(p, atomicAdd(p.counter, 1));
+        queue[s.pq] = s.pitem;
+    }
+}
+
+// One plane step of the current item.  FAST: every cell the tile computes
+// this item is interior (no Dirichlet masks, no trapezoid row skipping).
+// PH = g mod 3 selects the register rotation statically.  Returns true when
+// the item is finished.
+template <class C, bool FAST, bool AZ, int PH>
+__device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const JacobiParams& p,
+                                            double* ring, double* xb, uint64_t* full,
+                                            ItemInfo* queue, LevelQ<C> (&Q)[C::T], JState& s) {
+    constexpr int T = C::T, RJ = C::RJ, NW = C::NW, S = C::S, BW = C::BW;
+    constexpr int D = PH % 3, CC = (PH + 1) % 3, U = (PH + 2) % 3;
     const int tid = threadIdx.x;
-    const int tx = tid % C::TC, ty = tid / C::TC;
-    // smem column of this thread's first cell, smem row of its first row
-    const int c0 = C::H - C::HP + 2 * tx;
-    const int r0 = 1 + RJ * ty;
-    // offsets of this thread's cells relative to the tile origin
-    const int di = -C::HP + 2 * tx;        // i - I0 of the first cell
-    const int dj = -(T - 1) + RJ * ty;     // j - J0 of the first row
+    const int lane = tid & 31, w = tid >> 5;
+    const int col = 2 * lane;
+    const int brow = 1 + w * RJ;
+    const int di = col - C::H;
+    const int dj = -(T - 1) + w * RJ;
+    const ItemInfo& it = s.it;
 
-    // ---- producer state (thread 0 only) ------------------------------------
-    uint32_t ld_issued = 0;    // loads issued so far (slot = count % S)
-    int pq = 0;                // producer queue slot of its current item
-    ItemInfo pitem;
-    int pn = 0;                // producer's plane step within its item
+    const int slot = s.g % S, pslot = (s.g + S - 1) % S;
+    mbar_wait(&full[slot], (s.g / S) & 1);
+    const double* cur = ring + size_t(slot) * C::BOXS;
+    const double* prv = ring + size_t(pslot) * C::BOXS;
+    const int pplane = it.kb - T + s.n;
+    const int gi = it.I0 + di, gj = it.J0 + dj;
+    const bool in_i0 = (gi >= 1) && (gi <= p.ni);
+    const bool in_i1 = (gi + 1 >= 1) && (gi + 1 <= p.ni);
+    const double a = p.a, b = p.b;
 
-    if (tid == 0) {
-        tma_prefetch_desc(&src_map);
-        tma_prefetch_desc(&dst_map);
-        for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
-        fence_mbar_init();
-        pitem = decode_item<C>(p, atomicAdd(p.counter, 1));
-        queue[0] = pitem;
-        // prologue: fill S-1 ring slots
-        while (ld_issued < S - 1 && pitem.N > 0) {
-            uint64_t* bar = &full[ld_issued % S];
-            mbar_arrive_expect_tx(bar, C::BOX_BYTES);
-            tma_load_3d(ring + size_t(ld_issued % S) * PSTRIDE, &src_map, pitem.I0 - C::H,
-                        pitem.J0 - T, pitem.kb - T + pn, bar);
-            ++ld_issued;
-            if (++pn == pitem.N) {
-                pn = 0;
-                pq = (pq + 1) % C::QSLOTS;
-                pitem = decode_item<C>(p, atomicAdd(p.counter, 1));
-                queue[pq] = pitem;
+#pragma unroll
+    for (int r = 0; r < RJ; ++r) {
+        const double2 x = lds2(cur + (brow + r) * BW + col);
+        Q[0].q[U][r][0] = x.x;
+        Q[0].q[U][r][1] = x.y;
+    }
+
+#pragma unroll
+    for (int L = 1; L <= T; ++L) {
+        LevelQ<C>& In = Q[L - 1];
+        const int k = pplane - L;
+        double sT0, sT1, nB0, nB1;
+        if (L == 1) {
+            const double2 s2 = lds2(prv + (brow - 1) * BW + col);
+            const double2 n2 = lds2(prv + (brow + RJ) * BW + col);
+            sT0 = s2.x; sT1 = s2.y; nB0 = n2.x; nB1 = n2.y;
+        } else {
+            const double* xr = xb + (size_t((L - 2) * 2 + ((s.g + 1) & 1)) * NW) * C::XROW;
+            const double2 s2 = lds2(xr + max(w - 1, 0) * C::XROW + BW + col);
+            const double2 n2 = lds2(xr + min(w + 1, NW - 1) * C::XROW + col);
+            sT0 = s2.x; sT1 = s2.y; nB0 = n2.x; nB1 = n2.y;
+        }
+        double nv[RJ][2];
+#pragma unroll
+        for (int r = 0; r < RJ; ++r) {
+            const double c0 = In.q[CC][r][0], c1 = In.q[CC][r][1];
+            const double wv = __shfl_up_sync(0xffffffffu, c1, 1);    // cell i-1 (lane-1)
+            const double ev = __shfl_down_sync(0xffffffffu, c0, 1);  // cell i+2 (lane+1)
+            const double s0 = (r > 0) ? In.q[CC][r - 1][0] : sT0;
+            const double s1 = (r > 0) ? In.q[CC][r - 1][1] : sT1;
+            const double n0 = (r + 1 < RJ) ? In.q[CC][r + 1][0] : nB0;
+            const double n1 = (r + 1 < RJ) ? In.q[CC][r + 1][1] : nB1;
+            bool compute = true;
+            if (!FAST) {
+                const int jr = dj + r, need = T - L;
+                compute = (jr >= -need) && (jr < C::TJ + need) && (k >= 1) && (k <= p.nk) &&
+                          (gj + r >= 1) && (gj + r <= p.nj);
+            }
+            if (compute) {
+                double acc0 = __dadd_rn(wv, c1), acc1 = __dadd_rn(c0, ev);
+                acc0 = __dadd_rn(acc0, s0);
+                acc1 = __dadd_rn(acc1, s1);
+                acc0 = __dadd_rn(acc0, n0);
+                acc1 = __dadd_rn(acc1, n1);
+                acc0 = __dadd_rn(acc0, In.q[D][r][0]);
+                acc1 = __dadd_rn(acc1, In.q[D][r][1]);
+                acc0 = __dadd_rn(acc0, In.q[U][r][0]);
+                acc1 = __dadd_rn(acc1, In.q[U][r][1]);
+                const double o0 = jac_final<AZ>(a, b, c0, acc0);
+                const double o1 = jac_final<AZ>(a, b, c1, acc1);
+                if (FAST) {
+                    nv[r][0] = o0;
+                    nv[r][1] = o1;
+                } else {
+                    nv[r][0] = in_i0 ? o0 : c0;
+                    nv[r][1] = in_i1 ? o1 : c1;
+                }
+            } else {
+                nv[r][0] = c0;  // halo rows/planes keep their value; unneeded rows: anything
+                nv[r][1] = c1;
+            }
+        }
+        if (L < T) {
+            double* xw = xb + (size_t((L - 1) * 2 + (s.g & 1)) * NW + w) * C::XROW;
+            sts2(xw + col, nv[0][0], nv[0][1]);
+            sts2(xw + BW + col, nv[RJ - 1][0], nv[RJ - 1][1]);
+#pragma unroll
+            for (int r = 0; r < RJ; ++r) {
+                Q[L].q[U][r][0] = nv[r][0];
+                Q[L].q[U][r][1] = nv[r][1];
+            }
+        } else if (s.n >= 2 * T) {
+            if (di >= 0 && di < C::TO && gi + 1 <= p.ni + 1) {
+                const int64_t nip = p.ni + 2;
+                double* o = p.dst + ((int64_t)k * (p.nj + 2)) * nip + gi;
+#pragma unroll
+                for (int r = 0; r < RJ; ++r) {
+                    const int jr = dj + r;
+                    if (jr >= 0 && jr < C::TJ && gj + r <= p.nj)
+                        *reinterpret_cast<double2*>(o + (int64_t)(gj + r) * nip) =
+                            make_double2(nv[r][0], nv[r][1]);
+                }
             }
         }
     }
     __syncthreads();
+    if (tid == 0 && s.pitem.N > 0) produce<C>(src_map, p, ring, full, queue, s);
+    ++s.g;
+    return ++s.n == it.N;
+}
 
-    // ---- consumer state -----------------------------------------------------
-    // z-queues per level: level L values (L = 0..T-1) at planes k-1 (D) and k (C)
-    double qD[T][RJ][2], qC[T][RJ][2];
+// All plane steps of one item, entering the 3-phase rotation at g mod 3.
+template <class C, bool FAST, bool AZ>
+__device__ __forceinline__ void jacobi_item(const CUtensorMap* src_map, const JacobiParams& p,
+                                         double* ring, double* xb, uint64_t* full, ItemInfo* queue,
+                                         LevelQ<C> (&Q)[C::T], JState& s) {
+    const int ph = s.g % 3;
+    if (ph == 1) {
+        if (jacobi_step<C, FAST, AZ, 1>(src_map, p, ring, xb, full, queue, Q, s)) return;
+        if (jacobi_step<C, FAST, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s)) return;
+    } else if (ph == 2) {
+        if (jacobi_step<C, FAST, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s)) return;
+    }
+    while (true) {
+        if (jacobi_step<C, FAST, AZ, 0>(src_map, p, ring, xb, full, queue, Q, s)) return;
+        if (jacobi_step<C, FAST, AZ, 1>(src_map, p, ring, xb, full, queue, Q, s)) return;
+        if (jacobi_step<C, FAST, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s)) return;
+    }
+}
+
+template <class C, bool AZ>
+__global__ void __launch_bounds__(C::NT, C::MINB)
+jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map, const JacobiParams p) {
+    constexpr int T = C::T, S = C::S;
+    extern __shared__ __align__(128) double smem[];
+    double* ring = smem + C::RING_OFF;
+    double* xb = smem + C::X_OFF;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DBL_END);
+    ItemInfo* queue = reinterpret_cast<ItemInfo*>(full + S);
+    const int tid = threadIdx.x;
+
+    JState s;
+    s.ld_issued = 0;
+    s.pq = s.pn = 0;
+    s.pitem.N = 0;
+    if (tid == 0) {
+        tma_prefetch_desc(&src_map);
+        for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+        fence_mbar_init();
+        s.pitem = decode_item<C>(p, atomicAdd(p.counter, 1));
+        queue[0] = s.pitem;
+        while (s.ld_issued < S - 1 && s.pitem.N > 0) produce<C>(&src_map, p, ring, full, queue, s);
+    }
+    __syncthreads();
+
+    LevelQ<C> Q[T];
 #pragma unroll
     for (int L = 0; L < T; ++L)
 #pragma unroll
-        for (int r = 0; r < RJ; ++r) qD[L][r][0] = qD[L][r][1] = qC[L][r][0] = qC[L][r][1] = 0.0;
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int r = 0; r < C::RJ; ++r) Q[L].q[i][r][0] = Q[L].q[i][r][1] = 0.0;
 
-    uint32_t consumed = 0;  // global plane step counter
-    int cq = 0;             // consumer queue slot
-    ItemInfo it = queue[0];
-    int n = 0;              // plane step within the current item
-
-    while (it.N > 0) {
-        const int slot = consumed % S;
-        const int pslot = (consumed + S - 1) % S;
-        mbar_wait(&full[slot], (consumed / S) & 1);
-        const double* cur = ring + size_t(slot) * PSTRIDE;     // input plane p_n
-        const double* prv = ring + size_t(pslot) * PSTRIDE;    // input plane p_n - 1
-        const int pplane = it.kb - T + n;                      // newest input plane index
-
-        // in-plane interior masks for this thread's cells
-        const int gi = it.I0 + di, gj = it.J0 + dj;
-        bool in_i[2], in_j[RJ];
-        in_i[0] = (gi >= 1) && (gi <= p.ni);
-        in_i[1] = (gi + 1 >= 1) && (gi + 1 <= p.ni);
-#pragma unroll
-        for (int r = 0; r < RJ; ++r) in_j[r] = (gj + r >= 1) && (gj + r <= p.nj);
-
-        // level-0 values (own cells of the newest plane)
-        double v[RJ][2];
-#pragma unroll
-        for (int r = 0; r < RJ; ++r) {
-            const double2 x = *reinterpret_cast<const double2*>(cur + (r0 + r) * BW + c0);
-            v[r][0] = x.x;
-            v[r][1] = x.y;
-        }
-
-#pragma unroll
-        for (int L = 1; L <= T; ++L) {
-            const int kL = pplane - L;  // plane computed by level L at this step
-            const bool kin = (kL >= 1) && (kL <= p.nk);
-            // region of level L actually needed downstream: tile +- (T-L)
-            const int need = T - L;
-            const bool act = (di + 1 >= -need) && (di < C::TO + need) && (dj + RJ - 1 >= -need) &&
-                             (dj < TJ + need);
-            const double* src = (L == 1) ? prv : (lvl + size_t((L - 2) * 2 + ((consumed + 1) & 1)) * PSTRIDE);
-            double nv[RJ][2];
-            if (act) {
-#pragma unroll
-                for (int r = 0; r < RJ; ++r) {
-                    const double* row = src + (r0 + r) * BW + c0;
-                    const double w = row[-1];
-                    const double e = row[2];
-                    const double2 sv = *reinterpret_cast<const double2*>(row - BW);
-                    const double2 nn = *reinterpret_cast<const double2*>(row + BW);
-                    const double cc0 = qC[L - 1][r][0], cc1 = qC[L - 1][r][1];
-                    // cell 0: W = w, E = cc1 (own neighbour), cell 1: W = cc0, E = e
-                    double o0 = jac_cell(p.a, p.b, cc0, w, cc1, sv.x, nn.x, qD[L - 1][r][0], v[r][0]);
-                    double o1 = jac_cell(p.a, p.b, cc1, cc0, e, sv.y, nn.y, qD[L - 1][r][1], v[r][1]);
-                    const bool rowin = kin && in_j[r];
-                    nv[r][0] = (rowin && in_i[0]) ? o0 : cc0;
-                    nv[r][1] = (rowin && in_i[1]) ? o1 : cc1;
-                }
-            } else {
-#pragma unroll
-                for (int r = 0; r < RJ; ++r) nv[r][0] = nv[r][1] = 0.0;
-            }
-            if (L < T) {
-                if (act) {
-                    double* dst = lvl + size_t((L - 1) * 2 + (consumed & 1)) * PSTRIDE;
-#pragma unroll
-                    for (int r = 0; r < RJ; ++r)
-                        *reinterpret_cast<double2*>(dst + (r0 + r) * BW + c0) =
-                            make_double2(nv[r][0], nv[r][1]);
-                }
-            } else if (n >= 2 * T) {
-                // output tile cells: i - I0 in [0, TI), j - J0 in [0, TJ)
-                double* ob = outb + size_t(consumed & 1) * ((C::OUT + 15) / 16 * 16);
-                if (di >= 0 && di < C::TO) {
-#pragma unroll
-                    for (int r = 0; r < RJ; ++r) {
-                        const int jj = dj + r;
-                        if (jj >= 0 && jj < TJ)
-                            *reinterpret_cast<double2*>(ob + jj * C::TO + di) =
-                                make_double2(nv[r][0], nv[r][1]);
-                    }
-                }
-            }
-            // shift the level-(L-1) z-queue: D <- C <- (value at plane k+1)
-#pragma unroll
-            for (int r = 0; r < RJ; ++r) {
-                qD[L - 1][r][0] = qC[L - 1][r][0];
-                qD[L - 1][r][1] = qC[L - 1][r][1];
-                qC[L - 1][r][0] = v[r][0];
-                qC[L - 1][r][1] = v[r][1];
-                v[r][0] = nv[r][0];
-                v[r][1] = nv[r][1];
-            }
-        }
-        if (n >= 2 * T) fence_proxy_async_smem();
-        if (tid == 0) bulk_wait_read<0>();  // the previous output store has left smem
-        __syncthreads();
-
-        if (tid == 0) {
-            if (n >= 2 * T) {
-                const double* ob = outb + size_t(consumed & 1) * ((C::OUT + 15) / 16 * 16);
-                tma_store_3d(&dst_map, ob, it.I0, it.J0, pplane - T);
-                bulk_commit();
-            }
-            // refill the slot freed by this step (plane p_n - 1)
-            if (pitem.N > 0) {
-                uint64_t* bar = &full[ld_issued % S];
-                mbar_arrive_expect_tx(bar, C::BOX_BYTES);
-                tma_load_3d(ring + size_t(ld_issued % S) * PSTRIDE, &src_map, pitem.I0 - C::H,
-                            pitem.J0 - T, pitem.kb - T + pn, bar);
-                ++ld_issued;
-                if (++pn == pitem.N) {
-                    pn = 0;
-                    pq = (pq + 1) % C::QSLOTS;
-                    pitem = decode_item<C>(p, atomicAdd(p.counter, 1));
-                    queue[pq] = pitem;
-                }
-            }
-        }
-        ++consumed;
-        if (++n == it.N) {
-            n = 0;
-            // the producer wrote the next item before issuing its first load,
-            // which happened at least one barrier ago
-            __syncthreads();
-            cq = (cq + 1) % C::QSLOTS;
-            it = queue[cq];
-        }
+    s.g = 0;
+    s.n = 0;
+    s.cq = 0;
+    s.it = queue[0];
+    while (s.it.N > 0) {
+        // FAST when every cell computed for this item is interior: the input
+        // box (less its 1-cell rim) lies inside [1,ni] x [1,nj] for all planes
+        // [kb-T+1, ke+T-1)
+        const int ke = s.it.kb + s.it.N - 2 * T;
+        const bool fast = (s.it.I0 - C::H >= 1) && (s.it.I0 - C::H + C::BW - 1 <= p.ni) &&
+                          (s.it.J0 - (T - 1) >= 1) && (s.it.J0 - (T - 1) + C::ROWS - 1 <= p.nj) &&
+                          (s.it.kb - T + 1 >= 1) && (ke + T - 2 <= p.nk);
+        if (fast) jacobi_item<C, true, AZ>(&src_map, p, ring, xb, full, queue, Q, s);
+        else jacobi_item<C, false, AZ>(&src_map, p, ring, xb, full, queue, Q, s);
+        s.n = 0;
+        __syncthreads();  // queue[] entry written by thread 0 at least one barrier ago
+        s.cq = (s.cq + 1) % C::QSLOTS;
+        s.it = queue[s.cq];
     }
-    if (tid == 0) bulk_wait<0>();
 }
 
 }  // namespace sb

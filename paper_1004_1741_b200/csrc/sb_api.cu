@@ -179,15 +179,15 @@ __global__ void jacobi_generic_kernel(const double* __restrict__ src, double* __
 // ---------------------------------------------------------------------------
 // temporally blocked launch
 
-template <class C>
-static int launch_tb(const double* src, double* dst, int ni, int nj, int nk, int kfirst, int klast,
-                     double a, double b, cudaStream_t st) {
+template <class C, bool AZ>
+static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk, int kfirst,
+                          int klast, double a, double b, cudaStream_t st) {
     int* counters;
     int sms;
     int rc = get_counters(&counters, &sms);
     if (rc) return rc;
-    static int occ = -1;  // per template instantiation (same device type assumed)
-    auto kern = jacobi_tb_kernel<C>;
+    static int occ = -1;  // per instantiation (one device type per process)
+    auto kern = jacobi_tb_kernel<C, AZ>;
     if (occ < 0) {
         cudaError_t e =
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
@@ -198,22 +198,21 @@ static int launch_tb(const double* src, double* dst, int ni, int nj, int nk, int
         if (o < 1) return fail(SB_ERR_CUDA, "jacobi T=%d kernel does not fit on an SM", C::T);
         occ = o;
     }
-    CUtensorMap smap, dmap;
+    CUtensorMap smap;
     const int64_t nip = ni + 2, njp = nj + 2, nkp = nk + 2;
     if ((rc = make_grid_map(&smap, src, nip, njp, nkp, C::BW, C::BH))) return rc;
-    if ((rc = make_grid_map(&dmap, dst, nip, njp, nkp, C::TO, C::TJ))) return rc;
 
     JacobiParams p;
     p.ni = ni;
     p.nj = nj;
     p.nk = nk;
-    p.tiles_i = (ni + C::TI - 1) / C::TI;
+    p.tiles_i = (ni + 1 + C::TO - 1) / C::TO;  // tiles [TO*t, TO*t+TO) must cover [1, ni]
     p.tiles_j = (nj + C::TJ - 1) / C::TJ;
     const int grid = sms * occ;
     const int tiles = p.tiles_i * p.tiles_j;
     // k-block: aim for ~8 items per CTA, but never shorter than 8T planes
     // (each item re-reads 2T halo planes)
-    int want_items = grid * 8;
+    const int want_items = grid * 8;
     const int nkout = klast - kfirst;
     int kb = (int)(((int64_t)tiles * nkout + want_items - 1) / want_items);
     kb = max(kb, 8 * C::T);
@@ -226,38 +225,56 @@ static int launch_tb(const double* src, double* dst, int ni, int nj, int nk, int
     p.a = a;
     p.b = b;
     p.counter = counters;
+    p.dst = dst;
     cudaError_t e = cudaMemsetAsync(counters, 0, sizeof(int), st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counter)");
     const int nctas = min(grid, p.items);
-    kern<<<nctas, C::NT, C::SMEM_BYTES, st>>>(smap, dmap, p);
+    kern<<<nctas, C::NT, C::SMEM_BYTES, st>>>(smap, p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "jacobi_tb launch");
     return SB_OK;
 }
 
-// tile configurations per depth: <T, TI, TJ, RJ, S, MINB>
-using Cfg1 = JacobiCfg<1, 64, 16, 2, 4, 3>;
-using Cfg2 = JacobiCfg<2, 64, 16, 2, 4, 2>;
-using Cfg3 = JacobiCfg<3, 64, 8, 2, 3, 2>;
-using Cfg4 = JacobiCfg<4, 64, 8, 2, 3, 2>;
-using Cfg5 = JacobiCfg<5, 32, 8, 2, 3, 1>;
-using Cfg6 = JacobiCfg<6, 32, 8, 2, 3, 1>;
-using Cfg7 = JacobiCfg<7, 32, 8, 2, 3, 1>;
-using Cfg8 = JacobiCfg<8, 32, 8, 2, 3, 1>;
+
+template <class C>
+static int launch_tb(const double* src, double* dst, int ni, int nj, int nk, int kfirst, int klast,
+                     double a, double b, cudaStream_t st) {
+    if (a == 0.0) return launch_tb_impl<C, true>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+    return launch_tb_impl<C, false>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+}
+
+// tile configurations per depth: <T, RJ rows/thread, NW warps, S ring stages, MINB>
+// (SB_JCFG=<variant> selects alternatives during tuning)
+static int jcfg_variant() {
+    static int v = getenv("SB_JCFG") ? atoi(getenv("SB_JCFG")) : 0;
+    return v;
+}
 
 static int launch_depth(int T, const double* src, double* dst, int ni, int nj, int nk, int kfirst,
                         int klast, double a, double b, cudaStream_t st) {
     if (klast <= kfirst) return SB_OK;
+    const int v = jcfg_variant();
+#define SB_L(...) return launch_tb<JacobiCfg<__VA_ARGS__>>(src, dst, ni, nj, nk, kfirst, klast, a, b, st)
     switch (T) {
-        case 1: return launch_tb<Cfg1>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
-        case 2: return launch_tb<Cfg2>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
-        case 3: return launch_tb<Cfg3>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
-        case 4: return launch_tb<Cfg4>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
-        case 5: return launch_tb<Cfg5>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
-        case 6: return launch_tb<Cfg6>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
-        case 7: return launch_tb<Cfg7>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
-        case 8: return launch_tb<Cfg8>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+        case 1:
+            if (v == 1) SB_L(1, 2, 8, 4, 4);
+            SB_L(1, 4, 8, 4, 2);
+        case 2:
+            if (v == 1) SB_L(2, 2, 16, 4, 1);
+            SB_L(2, 4, 8, 4, 2);
+        case 3:
+            if (v == 1) SB_L(3, 4, 8, 4, 1);
+            SB_L(3, 2, 16, 4, 1);
+        case 4:
+            if (v == 1) SB_L(4, 4, 8, 4, 1);
+            if (v == 2) SB_L(4, 2, 16, 3, 1);
+            SB_L(4, 2, 16, 4, 1);
+        case 5: SB_L(5, 2, 12, 3, 1);
+        case 6: SB_L(6, 2, 12, 3, 1);
+        case 7: SB_L(7, 2, 12, 3, 1);
+        case 8: SB_L(8, 2, 12, 3, 1);
     }
+#undef SB_L
     return fail(SB_ERR_PLAN, "unsupported depth %d", T);
 }
 
