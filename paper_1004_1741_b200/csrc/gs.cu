@@ -8,35 +8,38 @@
 // Dependency structure.  Cell (k,j,i) of sweep s reads the sweep-s values
 // of its W, S, D neighbours and the sweep-(s-1) values of E, N, U.  Any
 // schedule that respects these edges reproduces the serial result bit for
-// bit as long as each cell's own arithmetic is identical, so the GPU is
-// free to run everything that is not ordered by them concurrently:
+// bit as long as each cell's own arithmetic is identical:
 //
 // * Inside a CTA, a tile of BJ x BK lines (rows j x planes k) is processed
-//   by one thread per line.  Line (jl, kl) is skewed by jl+kl steps: at
-//   local step t it updates cell i = 1 + t - (jl+kl).  Then S and D were
+//   by one compute thread per line.  Line (jl, kl) is skewed by jl+kl steps:
+//   at local step t it updates cell i = 1 + t - (jl+kl).  S and D were then
 //   produced one step earlier by the neighbouring lines, N and U are still
-//   untouched, and one __syncthreads per step orders everything.  This is
-//   the hyperplane wavefront of the paper's pipeline-parallel GS, at cell
-//   granularity.
-// * The tile's lines plus their halo lines live in shared memory as a ring
-//   of column chunks (CW columns x (BJ+2) x (BK+2) lines), filled by one TMA
-//   box load per chunk and written back by BK TMA box stores per chunk.
+//   untouched, and one named barrier per step (compute warps only) orders
+//   everything -- the hyperplane wavefront of the paper's pipeline-parallel
+//   GS at cell granularity.
+// * The tile's lines plus their halo lines live in shared memory as a ring of
+//   column chunks (CW columns x (BJ+2) x (BK+2) lines), filled by TMA box
+//   loads and written back by TMA box stores.
+// * A producer warp (warp specialisation) does everything that waits on
+//   other CTAs: polling neighbour progress, issuing chunk loads ahead of the
+//   compute, storing finished chunks and publishing progress.  The compute
+//   warps only ever wait on shared-memory mbarriers.
 // * Across CTAs, tile (J,K) of sweep s may load chunk c once
-//     - tiles (J-1,K), (J,K-1) of sweep s   have stored chunk c (new W/S/D),
+//     - tiles (J-1,K), (J,K-1) of sweep s          have stored chunk c,
 //     - tiles (J+1,K), (J,K+1), (J,K) of sweep s-1 have stored chunk c
 //       (old N/U/E, not yet overwritten: their sweep-s stores depend on us).
-//   Progress counters per (sweep mod R, tile) are published with
-//   st.release after the TMA store completed and polled with ld.acquire.
-// * Tasks (s, tile) are handed out by an atomic ticket in sweep-major,
-//   anti-diagonal (J+K) order, so a task only ever waits on tasks with a
-//   smaller ticket, which are already running: deadlock-free on a
-//   persistent grid, and successive sweeps pipeline behind each other like
-//   the paper's shifted wavefronts.
+//   Progress counters per (sweep mod R, tile) are published with st.release
+//   after the TMA stores completed and polled with ld.acquire.
+// * Tasks (sweep, tile) are handed out by an atomic ticket in sweep-major,
+//   anti-diagonal (J+K) order, so a task only waits on tasks with smaller
+//   tickets, which are already running: deadlock-free on a persistent grid,
+//   and successive sweeps pipeline behind each other like the paper's
+//   shifted wavefronts.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
-#include <cstdint>
 #include <algorithm>
+#include <cstdint>
 #include <vector>
 
 #include "../../include/stencil_b200.h"
@@ -45,8 +48,6 @@
 
 namespace sb {
 
-int make_grid_map(CUtensorMap* m, const double* base, int64_t nip, int64_t njp, int64_t nkp, int bw,
-                  int bh);
 int make_grid_map3(CUtensorMap* m, const double* base, int64_t nip, int64_t njp, int64_t nkp, int bw,
                    int bh, int bd);
 
@@ -54,7 +55,6 @@ struct GsParams {
     int ni, nj, nk;
     int tiles_j, tiles_k, ntiles;
     int nch;               // column chunks per line (ceil((ni+2)/CW))
-    int sweeps;            // sweeps in this launch
     long long tasks;       // sweeps * ntiles
     double b;
     int* ticket;           // atomic task counter
@@ -63,212 +63,263 @@ struct GsParams {
     const short2* order;   // ticket -> (J, K) within a sweep
 };
 
-template <int BJ_, int BK_, int CW_, int NS_, int MINB_>
+template <int BJ_, int BK_, int CW_, int NS_>
 struct GsCfg {
-    static constexpr int BJ = BJ_, BK = BK_, CW = CW_, NS = NS_, MINB = MINB_;
-    static constexpr int NT = BJ * BK;
+    static constexpr int BJ = BJ_, BK = BK_, CW = CW_, NS = NS_;
+    static constexpr int NCOMP = BJ * BK;                // compute threads (one per line)
+    static_assert(NCOMP % 32 == 0, "whole compute warps");
+    static constexpr int NT = NCOMP + 32;                // + one producer warp
     static constexpr int LJ = BJ + 2, LK = BK + 2;       // lines incl. halo
     static constexpr int LINES = LJ * LK;
     static constexpr int SLOT = CW * LINES;              // doubles per chunk slot
     static constexpr int SMAX = (BJ - 1) + (BK - 1);     // max line skew
     static constexpr int R = 4;                          // sweep slots for progress
+    static constexpr int QS = NS + 2;                    // task queue entries (tasks may be
+                                                         // as short as one chunk)
     static constexpr uint32_t BOX_BYTES = uint32_t(SLOT) * 8;
-    static constexpr size_t SMEM_BYTES = size_t(NS) * SLOT * 8 + 8 * NS + 64;
-    // prefetch distance (steps) before a chunk is first needed
-    static constexpr int DPF = CW;
-    static_assert((NS - 1) * CW > DPF + SMAX + 2, "too few chunk slots for the skew");
+    // chunks live at once: the leading line reads chunk (t+2)/CW while the
+    // trailing one still works in chunk (t-SMAX+1)/CW; +2 loading/storing
+    static_assert((NS - 2) * CW >= SMAX + 3, "too few chunk slots for the skew");
+    static constexpr size_t SMEM_BYTES = size_t(NS) * SLOT * 8 + 16 * NS + 16 * QS + 64;
+};
+
+struct GsTask {
+    int s, J, K, tile;  // s < 0: stop
 };
 
 // progress encoding: (sweep+1) * (nch+1) + chunks_stored   (0 = nothing)
 __device__ __forceinline__ int prog_val(int s, int chunks, int nch) { return (s + 1) * (nch + 1) + chunks; }
 
 template <class C>
-__device__ __forceinline__ bool wait_prog(const GsParams& p, int s, int tile, int need_chunks,
-                                          volatile int* abort_flag) {
+__device__ __forceinline__ bool prog_ready(const GsParams& p, int s, int tile, int need_chunks) {
     if (s < 0) return true;
-    const int* addr = p.prog + (s % C::R) * p.ntiles + tile;
-    const int want = prog_val(s, need_chunks, p.nch);
-    if (ld_acquire(addr) >= want) return true;
-    const long long t0 = clock64();
-    while (ld_acquire(addr) < want) {
-        if (*reinterpret_cast<volatile int*>(p.err)) return false;
-        if (clock64() - t0 > (1LL << 35)) {  // ~17 s: a dependency never arrived
-            atomicExch(p.err, 1);
-            return false;
-        }
-        __nanosleep(64);
+    return ld_acquire(p.prog + (s % C::R) * p.ntiles + tile) >= prog_val(s, need_chunks, p.nch);
+}
+
+template <class C>
+__device__ __forceinline__ bool deps_ready(const GsParams& p, const GsTask& t, int c) {
+    const int need = c + 1;
+    if (t.s > 0) {
+        if (!prog_ready<C>(p, t.s - 1, t.tile, need)) return false;
+        if (t.J + 1 < p.tiles_j && !prog_ready<C>(p, t.s - 1, t.tile + 1, need)) return false;
+        if (t.K + 1 < p.tiles_k && !prog_ready<C>(p, t.s - 1, t.tile + p.tiles_j, need)) return false;
     }
+    if (t.J > 0 && !prog_ready<C>(p, t.s, t.tile - 1, need)) return false;
+    if (t.K > 0 && !prog_ready<C>(p, t.s, t.tile - p.tiles_j, need)) return false;
     return true;
 }
 
-template <class C, bool INTERLEAVED>
-__global__ void __launch_bounds__(C::NT, C::MINB)
-gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
-               const __grid_constant__ CUtensorMap st_map, const GsParams p) {
-    constexpr int BJ = C::BJ, BK = C::BK, CW = C::CW, NS = C::NS, LJ = C::LJ;
-    extern __shared__ __align__(128) double smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(NS) * C::SLOT);
-    __shared__ int s_task[2];
-    __shared__ int s_abort;
-
-    const int tid = threadIdx.x;
-    const int jl = tid % BJ, kl = tid / BJ;
-    const int skew = jl + kl;
-    // line index in a chunk slot (halo lines at jl = -1, BJ and kl = -1, BK)
-    const int line = (kl + 1) * LJ + (jl + 1);
-    const double b = p.b;
-
-    if (tid == 0) {
-        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
-        fence_mbar_init();
-        tma_prefetch_desc(&ld_map);
-        tma_prefetch_desc(&st_map);
-        s_abort = 0;
+template <class C>
+__device__ __forceinline__ GsTask decode_task(const GsParams& p, long long tk) {
+    GsTask t;
+    if (tk >= p.tasks) {
+        t.s = -1;
+        t.J = t.K = t.tile = 0;
+        return t;
     }
-    uint32_t loads = 0;   // chunk loads issued by this CTA (slot = loads % NS) -- tid 0
-    uint32_t waits = 0;   // chunk loads consumed (mirror of loads on all threads)
-    int stores_committed = 0;  // tid 0
+    t.s = (int)(tk / p.ntiles);
+    const short2 jk = p.order[tk % p.ntiles];
+    t.J = jk.x;
+    t.K = jk.y;
+    t.tile = t.K * p.tiles_j + t.J;
+    return t;
+}
 
-    while (true) {
-        if (tid == 0) {
-            int tk = atomicAdd(p.ticket, 1);
-            s_task[0] = tk;
+// ---------------------------------------------------------------------------
+// producer (one thread): loads ahead, stores behind, publishes progress
+template <class C>
+__device__ void gs_producer(const CUtensorMap* ld_map, const CUtensorMap* st_map, const GsParams& p,
+                            double* ring, uint64_t* full, uint64_t* done, GsTask* queue) {
+    constexpr int NS = C::NS, CW = C::CW;
+    const int nch = p.nch;
+    GsTask lt = decode_task<C>(p, atomicAdd(p.ticket, 1));  // task being loaded
+    int lq = 0;
+    queue[0] = lt;
+    int lc = 0;                      // next chunk of lt to load
+    GsTask stt = lt;                 // task being stored
+    int sq = 0, sc = 0;              // its queue slot, next chunk to store
+    uint32_t gload = 0, gstore = 0;  // global chunk counters
+    int pending = 0;                 // committed store groups not yet published
+    long long t0 = clock64();
+    bool loads_done = (lt.s < 0);
+    bool stop_pending = loads_done;  // compute warps still to be released for the stop task
+
+    while (!(loads_done && !stop_pending && gstore == gload)) {
+        bool progress = false;
+        // 0. release the compute warps waiting for the stop task's first chunk
+        //    (complete that slot's barrier phase without data) once the slot is free
+        if (stop_pending && gload < gstore + NS) {
+            mbar_arrive(&full[gload % NS]);
+            stop_pending = false;
+            progress = true;
         }
-        __syncthreads();
-        const long long ticket = s_task[0];
-        if (ticket >= p.tasks || s_abort) break;
-        const int s = (int)(ticket / p.ntiles);
-        const short2 jk = p.order[ticket % p.ntiles];
-        const int J = jk.x, K = jk.y;
-        const int tile = K * p.tiles_j + J;
-        const int J0 = 1 + J * BJ, K0 = 1 + K * BK;  // padded origin of the tile's lines
-        const int nsteps = p.ni + C::SMAX;            // local steps until every line is done
-        const uint32_t base = waits;                  // first chunk load of this task
-
-        // tid 0: dependency-checked chunk loads
-        int next_load = 0;  // next chunk to load (tid 0)
-        auto issue_loads_upto = [&](int t) -> bool {
-            // load every chunk whose due step (c*CW - 2 - DPF) is <= t
-            while (next_load < p.nch && next_load * CW - 2 - C::DPF <= t) {
-                const int c = next_load;
-                bool ok = true;
-                ok = ok && (s == 0 || wait_prog<C>(p, s - 1, tile, c + 1, &s_abort));
-                if (J > 0) ok = ok && wait_prog<C>(p, s, tile - 1, c + 1, &s_abort);
-                if (K > 0) ok = ok && wait_prog<C>(p, s, tile - p.tiles_j, c + 1, &s_abort);
-                if (s > 0 && J + 1 < p.tiles_j) ok = ok && wait_prog<C>(p, s - 1, tile + 1, c + 1, &s_abort);
-                if (s > 0 && K + 1 < p.tiles_k)
-                    ok = ok && wait_prog<C>(p, s - 1, tile + p.tiles_j, c + 1, &s_abort);
-                if (!ok) return false;
-                fence_proxy_async_global();
-                // the slot's previous chunk must have left smem (its store read done)
-                bulk_wait_read<0>();
-                const uint32_t slot = loads % NS;
-                mbar_arrive_expect_tx(&full[slot], C::BOX_BYTES);
-                tma_load_3d(smem + size_t(slot) * C::SLOT, &ld_map, c * CW, J0 - 1, K0 - 1, &full[slot]);
-                ++loads;
-                ++next_load;
-            }
-            return true;
-        };
-
-        if (tid == 0) {
-            // a tile may run at most R-1 sweeps ahead of its own oldest unfinished sweep
-            bool ok = wait_prog<C>(p, s - (C::R - 1), tile, p.nch, &s_abort);
-            ok = ok && issue_loads_upto(-1);
-            if (!ok) s_abort = 1;
-        }
-        __syncthreads();
-        if (s_abort) break;
-
-        double w = 0.0;            // own previous (new) value: the W neighbour
-        int have = -1;             // highest chunk this thread has waited for (task-local)
-        int stored = 0;            // chunks stored (tid 0)
-        int published = 0;         // chunks published (tid 0)
-
-        for (int t = 0; t < nsteps; ++t) {
-            const int i = 1 + t - skew;  // padded column of this line's cell
-            // wait for the chunk holding column i+1 (the leading need of this line)
-            {
-                const int cneed = min(p.nch - 1, max(0, (i + 1) / CW));
-                while (have < cneed) {
-                    ++have;
-                    const uint32_t ld = base + have;
-                    mbar_wait(&full[ld % NS], (ld / NS) & 1);
+        // 1. store the oldest chunk the compute warps have finished
+        if (gstore < gload) {
+            const uint32_t slot = gstore % NS;
+            if (mbar_try_wait(&done[slot], (gstore / NS) & 1)) {
+                const double* base = ring + size_t(slot) * C::SLOT;
+                const int J0 = 1 + stt.J * C::BJ, K0 = 1 + stt.K * C::BK;
+                for (int q = 0; q < C::BK; ++q)
+                    tma_store_3d(st_map, base + ((q + 1) * C::LJ + 1) * CW, sc * CW, J0, K0 + q);
+                bulk_commit();
+                ++pending;
+                ++gstore;
+                ++sc;
+                progress = true;
+                if (sc == nch) {  // task finished: publish everything once it has landed
+                    bulk_wait<0>();
+                    fence_proxy_async_global();
+                    st_release(p.prog + (stt.s % C::R) * p.ntiles + stt.tile, prog_val(stt.s, nch, nch));
+                    pending = 0;
+                    sq = (sq + 1) % C::QS;
+                    stt = queue[sq];
+                    sc = 0;
+                } else if (pending > 1) {  // all but the newest group have landed
+                    bulk_wait<1>();
+                    fence_proxy_async_global();
+                    pending = 1;
+                    st_release(p.prog + (stt.s % C::R) * p.ntiles + stt.tile, prog_val(stt.s, sc - 1, nch));
                 }
             }
-            const bool active = (i >= 1) && (i <= p.ni) && (J0 + jl <= p.nj) && (K0 + kl <= p.nk);
-            if (active) {
-                auto at = [&](int ln, int col) -> double* {
-                    const int c = col / CW;
-                    const uint32_t ld = base + c;
-                    return smem + size_t(ld % NS) * C::SLOT + ln * CW + (col - c * CW);
-                };
-                if (i == 1) w = *at(line, 0);
-                const double e = *at(line, i + 1);
-                const double sv = *at(line - 1, i);
-                const double nv = *at(line + 1, i);
-                const double dv = *at(line - LJ, i);
-                const double uv = *at(line + LJ, i);
+        }
+        // 2. load the next chunk when its slot is free and its inputs are published
+        if (!loads_done && gload < gstore + NS) {
+            bool ok = (lc > 0) || prog_ready<C>(p, lt.s - (C::R - 1), lt.tile, nch);
+            ok = ok && deps_ready<C>(p, lt, lc);
+            if (ok) {
+                if (gload >= NS) bulk_wait_read<0>();  // the slot's previous chunk left smem
+                fence_proxy_async_global();
+                const uint32_t slot = gload % NS;
+                mbar_arrive_expect_tx(&full[slot], C::BOX_BYTES);
+                tma_load_3d(ring + size_t(slot) * C::SLOT, ld_map, lc * CW, lt.J * C::BJ, lt.K * C::BK,
+                            &full[slot]);
+                ++gload;
+                ++lc;
+                progress = true;
+                if (lc == nch) {
+                    lc = 0;
+                    lq = (lq + 1) % C::QS;
+                    lt = decode_task<C>(p, atomicAdd(p.ticket, 1));
+                    queue[lq] = lt;
+                    if (lt.s < 0) loads_done = stop_pending = true;
+                }
+            }
+        }
+        if (progress) {
+            t0 = clock64();
+        } else {
+            if (*reinterpret_cast<volatile int*>(p.err)) __trap();
+            if (clock64() - t0 > (1LL << 35)) {  // ~17 s without progress: never hang
+                atomicExch(p.err, 1);
+                __threadfence();
+                __trap();
+            }
+            __nanosleep(32);
+        }
+    }
+    bulk_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+template <class C, bool INTERLEAVED>
+__global__ void __launch_bounds__(C::NT, 1)
+gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
+               const __grid_constant__ CUtensorMap st_map, const GsParams p) {
+    constexpr int BJ = C::BJ, CW = C::CW, NS = C::NS, LJ = C::LJ;
+    extern __shared__ __align__(128) double smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(NS) * C::SLOT);
+    uint64_t* done = full + NS;
+    GsTask* queue = reinterpret_cast<GsTask*>(done + NS);
+    const int tid = threadIdx.x;
+
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&done[s], C::NCOMP);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (tid >= C::NCOMP) {  // producer warp
+        if (tid == C::NCOMP) {
+            tma_prefetch_desc(&ld_map);
+            tma_prefetch_desc(&st_map);
+            gs_producer<C>(&ld_map, &st_map, p, smem, full, done, queue);
+        }
+        return;
+    }
+
+    // compute thread: one line of the tile
+    const int jl = tid % BJ, kl = tid / BJ;
+    const int skew = jl + kl;
+    const int line = (kl + 1) * LJ + (jl + 1);
+    const double b = p.b;
+    const int nch = p.nch;
+    uint32_t gc = 0;  // global chunk index of the current task's chunk 0
+    int q = 0;
+    while (true) {
+        // the first chunk's full[] phase also publishes queue[q]
+        mbar_wait(&full[gc % NS], (gc / NS) & 1);
+        const GsTask t = queue[q];
+        if (t.s < 0) break;
+        const int J0 = 1 + t.J * BJ, K0 = 1 + t.K * C::BK;
+        const bool line_in = (J0 + jl <= p.nj) && (K0 + kl <= p.nk);
+        int have = 1;     // chunks of this task known to be loaded
+        int arrived = 0;  // chunks of this task this thread has released
+        double wv = 0.0;  // own previous value (W neighbour)
+        const int nsteps = p.ni + C::SMAX;
+        for (int st = 0; st < nsteps; ++st) {
+            const int i = 1 + st - skew;  // this line's column at this step
+            const int cneed = min(nch - 1, max(0, (i + 1) / CW));
+            while (have <= cneed) {  // chunk holding column i+1 must be loaded
+                const uint32_t g = gc + have;
+                mbar_wait(&full[g % NS], (g / NS) & 1);
+                ++have;
+            }
+            if (i >= 1 && i <= p.ni && line_in) {
+                const int ci = i / CW, ce = (i + 1) / CW;
+                double* sc = smem + size_t((gc + ci) % NS) * C::SLOT + (i - ci * CW);
+                double* own = sc + line * CW;
+                if (i == 1) wv = own[-1];  // column 0: the Dirichlet halo
+                const double e = smem[size_t((gc + ce) % NS) * C::SLOT + line * CW + (i + 1 - ce * CW)];
+                const double sv = sc[(line - 1) * CW];
+                const double nv = sc[(line + 1) * CW];
+                const double dv = sc[(line - LJ) * CW];
+                const double uv = sc[(line + LJ) * CW];
                 double x;
                 if (INTERLEAVED && p.ni >= 2) {
                     double tmp = __dadd_rn(e, sv);
                     tmp = __dadd_rn(tmp, nv);
                     tmp = __dadd_rn(tmp, dv);
                     tmp = __dadd_rn(tmp, uv);
-                    x = __dmul_rn(b, __dadd_rn(w, tmp));
+                    x = __dmul_rn(b, __dadd_rn(wv, tmp));
                 } else {
-                    double acc = __dadd_rn(w, e);
+                    double acc = __dadd_rn(wv, e);
                     acc = __dadd_rn(acc, sv);
                     acc = __dadd_rn(acc, nv);
                     acc = __dadd_rn(acc, dv);
                     acc = __dadd_rn(acc, uv);
                     x = __dmul_rn(b, acc);
                 }
-                *at(line, i) = x;
-                w = x;
+                *own = x;
+                wv = x;
             }
-            // chunks completed by this step: the trailing line passed their last column
-            const int trail_col = 1 + t - C::SMAX;
-            const bool last = (t == nsteps - 1);
-            int complete = last ? p.nch : max(0, (trail_col + 1) / CW);
-            const bool storing = complete > stored;  // uniform across the CTA
-            if (storing) fence_proxy_async_smem();
-            __syncthreads();
-            if (s_abort) break;  // set by tid 0 before this barrier
-            if (tid == 0) {
-                bool ok = true;
-                while (stored < complete) {
-                    const uint32_t ld = base + stored;
-                    const double* slot = smem + size_t(ld % NS) * C::SLOT;
-                    for (int q = 0; q < BK; ++q)
-                        tma_store_3d(&st_map, slot + ((q + 1) * LJ + 1) * CW, stored * CW, J0, K0 + q);
-                    bulk_commit();
-                    ++stores_committed;
-                    ++stored;
+            // release every chunk this line is finished with (all reads of a
+            // chunk by a line happen before that line finishes the chunk)
+            const int fin = (i >= p.ni) ? nch : max(0, (i + 1) / CW);
+            if (fin > arrived) {
+                fence_proxy_async_smem();  // our smem writes -> visible to the TMA store
+                while (arrived < fin) {
+                    mbar_arrive(&done[(gc + arrived) % NS]);
+                    ++arrived;
                 }
-                // publish what has fully landed (all but the most recent group)
-                if (published < stored - 1) {
-                    bulk_wait<1>();
-                    fence_proxy_async_global();
-                    published = stored - 1;
-                    st_release(p.prog + (s % C::R) * p.ntiles + tile, prog_val(s, published, p.nch));
-                }
-                if (last) {
-                    bulk_wait<0>();
-                    fence_proxy_async_global();
-                    published = stored;
-                    st_release(p.prog + (s % C::R) * p.ntiles + tile, prog_val(s, published, p.nch));
-                }
-                ok = issue_loads_upto(t);
-                if (!ok) s_abort = 1;
             }
+            named_bar_sync(1, C::NCOMP);
         }
-        waits = base + p.nch;
-        __syncthreads();
-        if (s_abort) break;
+        gc += nch;
+        q = (q + 1) % C::QS;
     }
-    (void)stores_committed;
-    if (tid == 0) bulk_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -304,11 +355,10 @@ __global__ void gs_serial_kernel(double* g, int ni, int nj, int nk, int sweeps, 
 }
 
 // ---------------------------------------------------------------------------
-using GsC = GsCfg<8, 8, 16, 4, 4>;
+using GsC = GsCfg<16, 16, 16, 5>;  // CW = 16: 128-B lines (TMA smem addresses must be 128-B aligned)
 
 struct GsScratch {
-    int dev = -1;
-    int* words = nullptr;      // ticket, err
+    int* words = nullptr;  // ticket, err
     int* prog = nullptr;
     size_t prog_cap = 0;
     short2* order = nullptr;
@@ -317,20 +367,9 @@ struct GsScratch {
 };
 static GsScratch g_gs[16];
 
-int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,
-           cudaStream_t st) {
-    const bool inter = (kernel == SB_KERNEL_GS_INTERLEAVED);
-    if (!tma_ok(grid, ni)) {
-        for (int64_t done = 0; done < iters;) {
-            int n = (int)std::min<int64_t>(iters - done, 1 << 20);
-            if (inter) gs_serial_kernel<true><<<1, 32, 0, st>>>(grid, ni, nj, nk, n, b);
-            else gs_serial_kernel<false><<<1, 32, 0, st>>>(grid, ni, nj, nk, n, b);
-            done += n;
-        }
-        cudaError_t e = cudaGetLastError();
-        return e == cudaSuccess ? SB_OK : cuda_fail(e, "gs_serial launch");
-    }
-    using C = GsC;
+template <class C>
+static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double b, bool inter,
+                     cudaStream_t st) {
     int dev;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
@@ -342,11 +381,11 @@ int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int ke
     if (rc) return rc;
 
     const int tiles_j = (nj + C::BJ - 1) / C::BJ, tiles_k = (nk + C::BK - 1) / C::BK;
+    if (tiles_j > 32767 || tiles_k > 32767) return fail(SB_ERR_DIMENSION, "grid too large for GS tiling");
     const int ntiles = tiles_j * tiles_k;
-    if (!S.words) {
-        if ((e = cudaMalloc(&S.words, 64 * sizeof(int))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-    }
-    size_t need = size_t(C::R) * ntiles;
+    if (!S.words && (e = cudaMalloc(&S.words, 64 * sizeof(int))) != cudaSuccess)
+        return cuda_fail(e, "cudaMalloc");
+    const size_t need = size_t(C::R) * ntiles;
     if (S.prog_cap < need) {
         if (S.prog) cudaFree(S.prog);
         if ((e = cudaMalloc(&S.prog, need * sizeof(int))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
@@ -358,7 +397,7 @@ int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int ke
         ord.reserve(ntiles);
         for (int d = 0; d <= tiles_j + tiles_k - 2; ++d)
             for (int J = 0; J < tiles_j; ++J) {
-                int K = d - J;
+                const int K = d - J;
                 if (K >= 0 && K < tiles_k) ord.push_back(make_short2((short)J, (short)K));
             }
         if (S.order_cap < (size_t)ntiles) {
@@ -373,7 +412,6 @@ int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int ke
         S.tj = tiles_j;
         S.tk = tiles_k;
     }
-    if (tiles_j > 32767 || tiles_k > 32767) return fail(SB_ERR_DIMENSION, "grid too large for GS tiling");
 
     CUtensorMap lmap, smap;
     const int64_t nip = ni + 2, njp = nj + 2, nkp = nk + 2;
@@ -408,7 +446,6 @@ int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int ke
     const int64_t max_sweeps = ((int64_t(1) << 30) / (p.nch + 1)) - 2;
     for (int64_t done = 0; done < iters;) {
         const int n = (int)std::min<int64_t>(iters - done, max_sweeps);
-        p.sweeps = n;
         p.tasks = (long long)n * ntiles;
         if ((e = cudaMemsetAsync(S.words, 0, 64 * sizeof(int), st)) != cudaSuccess)
             return cuda_fail(e, "memset");
@@ -421,6 +458,22 @@ int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int ke
         done += n;
     }
     return SB_OK;
+}
+
+int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,
+           cudaStream_t st) {
+    const bool inter = (kernel == SB_KERNEL_GS_INTERLEAVED);
+    if (!tma_ok(grid, ni)) {
+        for (int64_t done = 0; done < iters;) {
+            const int n = (int)std::min<int64_t>(iters - done, 1 << 20);
+            if (inter) gs_serial_kernel<true><<<1, 32, 0, st>>>(grid, ni, nj, nk, n, b);
+            else gs_serial_kernel<false><<<1, 32, 0, st>>>(grid, ni, nj, nk, n, b);
+            done += n;
+        }
+        cudaError_t e = cudaGetLastError();
+        return e == cudaSuccess ? SB_OK : cuda_fail(e, "gs_serial launch");
+    }
+    return gs_launch<GsC>(grid, ni, nj, nk, iters, b, inter, st);
 }
 
 // error word readback (host) -- called by the synchronous entry points

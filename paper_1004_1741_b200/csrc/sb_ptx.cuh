@@ -114,4 +114,9 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 }
 __device__ __forceinline__ long long clock64_() { return clock64(); }
 
+// named barrier over `count` threads (a subset of the CTA, e.g. compute warps)
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 }  // namespace sb
