@@ -20,16 +20,18 @@
 // * The tile's lines plus their halo lines live in shared memory as a ring of
 //   column chunks (CW columns x (BJ+2) x (BK+2) lines), filled by TMA box
 //   loads and written back by TMA box stores.
-// * A producer warp (warp specialisation) does everything that waits on
-//   other CTAs: polling neighbour progress, issuing chunk loads ahead of the
-//   compute, storing finished chunks and publishing progress.  The compute
-//   warps only ever wait on shared-memory mbarriers.
+// * Warp specialisation: a loader warp polls neighbour progress (with a
+//   cache of the last value seen) and issues chunk loads ahead of the
+//   compute; a storer warp writes finished chunks back, frees their ring
+//   slot once the store has read shared memory and publishes progress once
+//   it has landed.  The compute warps only wait on shared-memory mbarriers,
+//   at CTA-uniform steps.
 // * Across CTAs, tile (J,K) of sweep s may load chunk c once
 //     - tiles (J-1,K), (J,K-1) of sweep s          have stored chunk c,
 //     - tiles (J+1,K), (J,K+1), (J,K) of sweep s-1 have stored chunk c
 //       (old N/U/E, not yet overwritten: their sweep-s stores depend on us).
 //   Progress counters per (sweep mod R, tile) are published with st.release
-//   after the TMA stores completed and polled with ld.acquire.
+//   after the TMA store completed and polled with ld.acquire.
 // * Tasks (sweep, tile) are handed out by an atomic ticket in sweep-major,
 //   anti-diagonal (J+K) order, so a task only waits on tasks with smaller
 //   tickets, which are already running: deadlock-free on a persistent grid,
@@ -61,6 +63,7 @@ struct GsParams {
     int* prog;             // [R][ntiles] progress (encoded)
     int* err;              // error word (timeout)
     const short2* order;   // ticket -> (J, K) within a sweep
+    double* grid;          // the grid (results are written back directly)
 };
 
 template <int BJ_, int BK_, int CW_, int NS_>
@@ -68,19 +71,20 @@ struct GsCfg {
     static constexpr int BJ = BJ_, BK = BK_, CW = CW_, NS = NS_;
     static constexpr int NCOMP = BJ * BK;                // compute threads (one per line)
     static_assert(NCOMP % 32 == 0, "whole compute warps");
-    static constexpr int NT = NCOMP + 32;                // + one producer warp
+    static constexpr int NT = NCOMP + 64;                // + loader warp + storer warp
     static constexpr int LJ = BJ + 2, LK = BK + 2;       // lines incl. halo
     static constexpr int LINES = LJ * LK;
     static constexpr int SLOT = CW * LINES;              // doubles per chunk slot
     static constexpr int SMAX = (BJ - 1) + (BK - 1);     // max line skew
     static constexpr int R = 4;                          // sweep slots for progress
-    static constexpr int QS = NS + 2;                    // task queue entries (tasks may be
+    static constexpr int QS = NS + 4;                    // task queue entries (tasks may be
                                                          // as short as one chunk)
     static constexpr uint32_t BOX_BYTES = uint32_t(SLOT) * 8;
-    // chunks live at once: the leading line reads chunk (t+2)/CW while the
-    // trailing one still works in chunk (t-SMAX+1)/CW; +2 loading/storing
+    // chunks in use at once: leading line's E chunk down to the trailing
+    // line's chunk (the rest of the ring is prefetch)
     static_assert((NS - 2) * CW >= SMAX + 3, "too few chunk slots for the skew");
-    static constexpr size_t SMEM_BYTES = size_t(NS) * SLOT * 8 + 16 * NS + 16 * QS + 64;
+    static constexpr size_t SMEM_BYTES = size_t(NS) * SLOT * 8 + 24 * NS + 16 * QS + 64;
+    // (full[NS], empty[NS], one spare barrier row, task queue)
 };
 
 struct GsTask {
@@ -96,17 +100,45 @@ __device__ __forceinline__ bool prog_ready(const GsParams& p, int s, int tile, i
     return ld_acquire(p.prog + (s % C::R) * p.ntiles + tile) >= prog_val(s, need_chunks, p.nch);
 }
 
+// Dependencies of one task, with the last progress value observed for each
+// (a neighbour is usually several chunks ahead, so most checks hit the cache
+// and the loader issues no global load at all).
+struct GsDeps {
+    const int* addr[6];
+    int want_base[6];  // prog_val(sweep, 0, nch) of the awaited sweep
+    int seen[6];
+    int n;
+};
+
 template <class C>
-__device__ __forceinline__ bool deps_ready(const GsParams& p, const GsTask& t, int c) {
-    const int need = c + 1;
+__device__ __forceinline__ void deps_init(const GsParams& p, const GsTask& t, GsDeps& d) {
+    d.n = 0;
+    auto add = [&](int s, int tile) {
+        d.addr[d.n] = p.prog + (s % C::R) * p.ntiles + tile;
+        d.want_base[d.n] = prog_val(s, 0, p.nch);
+        d.seen[d.n] = 0;
+        ++d.n;
+    };
     if (t.s > 0) {
-        if (!prog_ready<C>(p, t.s - 1, t.tile, need)) return false;
-        if (t.J + 1 < p.tiles_j && !prog_ready<C>(p, t.s - 1, t.tile + 1, need)) return false;
-        if (t.K + 1 < p.tiles_k && !prog_ready<C>(p, t.s - 1, t.tile + p.tiles_j, need)) return false;
+        add(t.s - 1, t.tile);
+        if (t.J + 1 < p.tiles_j) add(t.s - 1, t.tile + 1);
+        if (t.K + 1 < p.tiles_k) add(t.s - 1, t.tile + p.tiles_j);
     }
-    if (t.J > 0 && !prog_ready<C>(p, t.s, t.tile - 1, need)) return false;
-    if (t.K > 0 && !prog_ready<C>(p, t.s, t.tile - p.tiles_j, need)) return false;
-    return true;
+    if (t.J > 0) add(t.s, t.tile - 1);
+    if (t.K > 0) add(t.s, t.tile - p.tiles_j);
+}
+
+// true when chunk c of the task may be loaded; polls only stale entries
+__device__ __forceinline__ bool deps_ready(GsDeps& d, int c) {
+    bool ok = true;
+    for (int k = 0; k < d.n; ++k) {
+        const int want = d.want_base[k] + c + 1;
+        if (d.seen[k] < want) {
+            d.seen[k] = ld_acquire(d.addr[k]);
+            ok = ok && (d.seen[k] >= want);
+        }
+    }
+    return ok;
 }
 
 template <class C>
@@ -125,99 +157,91 @@ __device__ __forceinline__ GsTask decode_task(const GsParams& p, long long tk) {
     return t;
 }
 
+__device__ __forceinline__ void gs_check_abort(const GsParams& p, long long& t0) {
+    if (*reinterpret_cast<volatile int*>(p.err)) __trap();
+    if (clock64() - t0 > (1LL << 35)) {  // ~17 s without progress: never hang
+        atomicExch(p.err, 1);
+        __threadfence();
+        __trap();
+    }
+    __nanosleep(64);
+}
+
 // ---------------------------------------------------------------------------
-// producer (one thread): loads ahead, stores behind, publishes progress
+// loader (one thread): dependency-checked chunk loads into free ring slots
 template <class C>
-__device__ void gs_producer(const CUtensorMap* ld_map, const CUtensorMap* st_map, const GsParams& p,
-                            double* ring, uint64_t* full, uint64_t* done, GsTask* queue) {
+__device__ void gs_loader(const CUtensorMap* ld_map, const GsParams& p, double* ring, uint64_t* full,
+                          uint64_t* empty, GsTask* queue) {
     constexpr int NS = C::NS, CW = C::CW;
     const int nch = p.nch;
-    GsTask lt = decode_task<C>(p, atomicAdd(p.ticket, 1));  // task being loaded
+    uint32_t gload = 0;
     int lq = 0;
-    queue[0] = lt;
-    int lc = 0;                      // next chunk of lt to load
-    GsTask stt = lt;                 // task being stored
-    int sq = 0, sc = 0;              // its queue slot, next chunk to store
-    uint32_t gload = 0, gstore = 0;  // global chunk counters
-    int pending = 0;                 // committed store groups not yet published
     long long t0 = clock64();
-    bool loads_done = (lt.s < 0);
-    bool stop_pending = loads_done;  // compute warps still to be released for the stop task
-
-    while (!(loads_done && !stop_pending && gstore == gload)) {
-        bool progress = false;
-        // 0. release the compute warps waiting for the stop task's first chunk
-        //    (complete that slot's barrier phase without data) once the slot is free
-        if (stop_pending && gload < gstore + NS) {
-            mbar_arrive(&full[gload % NS]);
-            stop_pending = false;
-            progress = true;
+    while (true) {
+        const GsTask lt = decode_task<C>(p, atomicAdd(p.ticket, 1));
+        queue[lq] = lt;  // published to the other warps by the next full[] phase
+        lq = (lq + 1) % C::QS;
+        const uint32_t slot0 = gload % NS;
+        if (lt.s < 0) {
+            // release the compute warps waiting for this (stop) task's first
+            // chunk: complete that slot's barrier phase without data
+            if (gload >= NS) mbar_wait(&empty[slot0], ((gload - NS) / NS) & 1);
+            mbar_arrive(&full[slot0]);
+            return;
         }
-        // 1. store the oldest chunk the compute warps have finished
-        if (gstore < gload) {
-            const uint32_t slot = gstore % NS;
-            if (mbar_try_wait(&done[slot], (gstore / NS) & 1)) {
-                const double* base = ring + size_t(slot) * C::SLOT;
-                const int J0 = 1 + stt.J * C::BJ, K0 = 1 + stt.K * C::BK;
-                for (int q = 0; q < C::BK; ++q)
-                    tma_store_3d(st_map, base + ((q + 1) * C::LJ + 1) * CW, sc * CW, J0, K0 + q);
-                bulk_commit();
-                ++pending;
-                ++gstore;
-                ++sc;
-                progress = true;
-                if (sc == nch) {  // task finished: publish everything once it has landed
-                    bulk_wait<0>();
-                    fence_proxy_async_global();
-                    st_release(p.prog + (stt.s % C::R) * p.ntiles + stt.tile, prog_val(stt.s, nch, nch));
-                    pending = 0;
-                    sq = (sq + 1) % C::QS;
-                    stt = queue[sq];
-                    sc = 0;
-                } else if (pending > 1) {  // all but the newest group have landed
-                    bulk_wait<1>();
-                    fence_proxy_async_global();
-                    pending = 1;
-                    st_release(p.prog + (stt.s % C::R) * p.ntiles + stt.tile, prog_val(stt.s, sc - 1, nch));
-                }
+        GsDeps deps;
+        deps_init<C>(p, lt, deps);
+        for (int c = 0; c < nch; ++c, ++gload) {
+            const uint32_t slot = gload % NS;
+            if (gload >= NS) {  // the slot's previous chunk must have been stored
+                while (!mbar_try_wait(&empty[slot], ((gload - NS) / NS) & 1)) gs_check_abort(p, t0);
             }
-        }
-        // 2. load the next chunk when its slot is free and its inputs are published
-        if (!loads_done && gload < gstore + NS) {
-            bool ok = (lc > 0) || prog_ready<C>(p, lt.s - (C::R - 1), lt.tile, nch);
-            ok = ok && deps_ready<C>(p, lt, lc);
-            if (ok) {
-                if (gload >= NS) bulk_wait_read<0>();  // the slot's previous chunk left smem
-                fence_proxy_async_global();
-                const uint32_t slot = gload % NS;
-                mbar_arrive_expect_tx(&full[slot], C::BOX_BYTES);
-                tma_load_3d(ring + size_t(slot) * C::SLOT, ld_map, lc * CW, lt.J * C::BJ, lt.K * C::BK,
-                            &full[slot]);
-                ++gload;
-                ++lc;
-                progress = true;
-                if (lc == nch) {
-                    lc = 0;
-                    lq = (lq + 1) % C::QS;
-                    lt = decode_task<C>(p, atomicAdd(p.ticket, 1));
-                    queue[lq] = lt;
-                    if (lt.s < 0) loads_done = stop_pending = true;
-                }
-            }
-        }
-        if (progress) {
+            while (!((c > 0 || prog_ready<C>(p, lt.s - (C::R - 1), lt.tile, nch)) && deps_ready(deps, c)))
+                gs_check_abort(p, t0);
             t0 = clock64();
-        } else {
-            if (*reinterpret_cast<volatile int*>(p.err)) __trap();
-            if (clock64() - t0 > (1LL << 35)) {  // ~17 s without progress: never hang
-                atomicExch(p.err, 1);
-                __threadfence();
-                __trap();
-            }
-            __nanosleep(32);
+            fence_proxy_async_global();
+            mbar_arrive_expect_tx(&full[slot], C::BOX_BYTES);
+            tma_load_3d(ring + size_t(slot) * C::SLOT, ld_map, c * CW, lt.J * C::BJ, lt.K * C::BK,
+                        &full[slot]);
         }
     }
-    bulk_wait<0>();
+}
+
+// storer (one thread): writes finished chunks back with TMA, frees the ring
+// slot as soon as the store has read shared memory, and publishes progress
+// once the data has landed in global memory
+template <class C>
+__device__ void gs_storer(const CUtensorMap* st_map, const GsParams& p, double* ring, uint64_t* done,
+                          uint64_t* empty, uint64_t* full, GsTask* queue) {
+    constexpr int NS = C::NS, CW = C::CW;
+    const int nch = p.nch;
+    uint32_t gstore = 0;
+    int sq = 0;
+    long long t0 = clock64();
+    while (true) {
+        // the task's first chunk being loaded implies its queue entry is written
+        const uint32_t slot0 = gstore % NS;
+        while (!mbar_try_wait(&full[slot0], (gstore / NS) & 1)) gs_check_abort(p, t0);
+        const GsTask t = queue[sq];
+        sq = (sq + 1) % C::QS;
+        if (t.s < 0) return;
+        const int J0 = 1 + t.J * C::BJ, K0 = 1 + t.K * C::BK;
+        int* flag = p.prog + (t.s % C::R) * p.ntiles + t.tile;
+        for (int c = 0; c < nch; ++c, ++gstore) {
+            const uint32_t slot = gstore % NS;
+            while (!mbar_try_wait(&done[slot], (gstore / NS) & 1)) gs_check_abort(p, t0);
+            t0 = clock64();
+            const double* base = ring + size_t(slot) * C::SLOT;
+            for (int q = 0; q < C::BK; ++q)
+                tma_store_3d(st_map, base + ((q + 1) * C::LJ + 1) * CW, c * CW, J0, K0 + q);
+            bulk_commit();
+            bulk_wait_read<0>();  // the slot's data has left shared memory
+            mbar_arrive(&empty[slot]);
+            bulk_wait<0>();       // ... and landed in global memory
+            fence_proxy_async_global();
+            st_release(flag, prog_val(t.s, c + 1, nch));
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -225,70 +249,75 @@ template <class C, bool INTERLEAVED>
 __global__ void __launch_bounds__(C::NT, 1)
 gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
                const __grid_constant__ CUtensorMap st_map, const GsParams p) {
-    constexpr int BJ = C::BJ, CW = C::CW, NS = C::NS, LJ = C::LJ;
+    constexpr int BJ = C::BJ, CW = C::CW, NS = C::NS, LJ = C::LJ, SMAX = C::SMAX;
     extern __shared__ __align__(128) double smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(NS) * C::SLOT);
     uint64_t* done = full + NS;
-    GsTask* queue = reinterpret_cast<GsTask*>(done + NS);
+    uint64_t* empty = done + NS;
+    GsTask* queue = reinterpret_cast<GsTask*>(empty + NS);
     const int tid = threadIdx.x;
 
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&done[s], C::NCOMP);
+            mbar_init(&done[s], 1);
+            mbar_init(&empty[s], 1);
         }
         fence_mbar_init();
     }
     __syncthreads();
 
-    if (tid >= C::NCOMP) {  // producer warp
+    if (tid >= C::NCOMP) {
         if (tid == C::NCOMP) {
             tma_prefetch_desc(&ld_map);
+            gs_loader<C>(&ld_map, p, smem, full, empty, queue);
+        } else if (tid == C::NCOMP + 32) {
             tma_prefetch_desc(&st_map);
-            gs_producer<C>(&ld_map, &st_map, p, smem, full, done, queue);
+            gs_storer<C>(&st_map, p, smem, done, empty, full, queue);
         }
         return;
     }
 
-    // compute thread: one line of the tile
+    // compute thread: one line of the tile.  All chunk waits and releases are
+    // CTA-uniform events (functions of the step only), handled by thread 0
+    // around the per-step named barrier: when the trailing line completes a
+    // chunk, every thread fences its shared-memory writes for the async proxy
+    // and after the barrier thread 0 hands the chunk to the storer.
     const int jl = tid % BJ, kl = tid / BJ;
     const int skew = jl + kl;
     const int line = (kl + 1) * LJ + (jl + 1);
     const double b = p.b;
-    const int nch = p.nch;
+    const int nch = p.nch, ni = p.ni;
+    const int nsteps = ni + SMAX;
     uint32_t gc = 0;  // global chunk index of the current task's chunk 0
     int q = 0;
     while (true) {
-        // the first chunk's full[] phase also publishes queue[q]
-        mbar_wait(&full[gc % NS], (gc / NS) & 1);
+        if (tid == 0) mbar_wait(&full[gc % NS], (gc / NS) & 1);  // chunk 0 (+ queue entry)
+        named_bar_sync(1, C::NCOMP);
         const GsTask t = queue[q];
+        q = (q + 1) % C::QS;
         if (t.s < 0) break;
         const int J0 = 1 + t.J * BJ, K0 = 1 + t.K * C::BK;
         const bool line_in = (J0 + jl <= p.nj) && (K0 + kl <= p.nk);
-        int have = 1;     // chunks of this task known to be loaded
-        int arrived = 0;  // chunks of this task this thread has released
-        double wv = 0.0;  // own previous value (W neighbour)
-        const int nsteps = p.ni + C::SMAX;
-        for (int st = 0; st < nsteps; ++st) {
-            const int i = 1 + st - skew;  // this line's column at this step
-            const int cneed = min(nch - 1, max(0, (i + 1) / CW));
-            while (have <= cneed) {  // chunk holding column i+1 must be loaded
-                const uint32_t g = gc + have;
-                mbar_wait(&full[g % NS], (g / NS) & 1);
-                ++have;
+        // column i of this line at pi, column i+1 at pe
+        int i = 1 - skew;
+        double* pi = smem + size_t(gc % NS) * C::SLOT + line * CW + max(i, 0);
+        double* pe = pi + 1;
+        int ce = 0;                  // chunk of pe
+        double wv = pi[-max(i, 0)];  // column 0: the Dirichlet halo (W of column 1)
+        int ready = 1;       // chunks known loaded (thread 0's view, CTA-wide)
+        int completed = 0;   // chunks completed so far
+        int released = 0;    // chunks handed to the storer (thread 0)
+        for (int st = 0; st < nsteps; ++st, ++i) {
+            if (tid == 0) {  // every thread fenced its writes before the last barrier
+                while (released < completed) mbar_arrive(&done[(gc + released++) % NS]);
             }
-            if (i >= 1 && i <= p.ni && line_in) {
-                const int ci = i / CW, ce = (i + 1) / CW;
-                double* sc = smem + size_t((gc + ci) % NS) * C::SLOT + (i - ci * CW);
-                double* own = sc + line * CW;
-                if (i == 1) wv = own[-1];  // column 0: the Dirichlet halo
-                const double e = smem[size_t((gc + ce) % NS) * C::SLOT + line * CW + (i + 1 - ce * CW)];
-                const double sv = sc[(line - 1) * CW];
-                const double nv = sc[(line + 1) * CW];
-                const double dv = sc[(line - LJ) * CW];
-                const double uv = sc[(line + LJ) * CW];
+            if (i >= 1 && i <= ni && line_in) {
+                const double e = *pe;
+                const double sv = pi[-CW], nv = pi[CW];
+                const double dv = pi[-LJ * CW], uv = pi[LJ * CW];
                 double x;
-                if (INTERLEAVED && p.ni >= 2) {
+                if (INTERLEAVED && ni >= 2) {
                     double tmp = __dadd_rn(e, sv);
                     tmp = __dadd_rn(tmp, nv);
                     tmp = __dadd_rn(tmp, dv);
@@ -302,23 +331,39 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
                     acc = __dadd_rn(acc, uv);
                     x = __dmul_rn(b, acc);
                 }
-                *own = x;
+                *pi = x;
                 wv = x;
             }
-            // release every chunk this line is finished with (all reads of a
-            // chunk by a line happen before that line finishes the chunk)
-            const int fin = (i >= p.ni) ? nch : max(0, (i + 1) / CW);
-            if (fin > arrived) {
-                fence_proxy_async_smem();  // our smem writes -> visible to the TMA store
-                while (arrived < fin) {
-                    mbar_arrive(&done[(gc + arrived) % NS]);
-                    ++arrived;
+            if (i >= 0) {  // advance: pi to column i+1, pe to column i+2
+                pi = pe;
+                if ((i + 2) % CW == 0 && i + 2 < nch * CW) {
+                    ++ce;
+                    pe = smem + size_t((gc + ce) % NS) * C::SLOT + line * CW;
+                } else {
+                    ++pe;
+                }
+            }
+            // trailing line (skew SMAX) just finished column st+1-SMAX: chunks
+            // below that are complete; the last step completes everything
+            const int fin = (st == nsteps - 1) ? nch : min(nch, max(0, (st + 2 - SMAX) / CW));
+            if (fin > completed) {
+                fence_proxy_async_smem();  // this thread's smem writes -> async proxy
+                completed = fin;           // released after this step's barrier
+            }
+            // the leading line (skew 0) reads column st+3 next step
+            if (tid == 0) {
+                const int cneed = (st + 3) / CW;
+                if (cneed < nch && cneed >= ready) {
+                    mbar_wait(&full[(gc + cneed) % NS], ((gc + cneed) / NS) & 1);
+                    ready = cneed + 1;
                 }
             }
             named_bar_sync(1, C::NCOMP);
         }
+        if (tid == 0) {
+            while (released < completed) mbar_arrive(&done[(gc + released++) % NS]);
+        }
         gc += nch;
-        q = (q + 1) % C::QS;
     }
 }
 
@@ -442,6 +487,7 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
     p.err = S.words + 1;
     p.prog = S.prog;
     p.order = S.order;
+    p.grid = grid;
     // sweeps per launch bounded by the int32 progress encoding
     const int64_t max_sweeps = ((int64_t(1) << 30) / (p.nch + 1)) - 2;
     for (int64_t done = 0; done < iters;) {

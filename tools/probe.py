@@ -37,7 +37,7 @@ def main():
     sp = ctypes.c_void_p(st.cuda_stream)
     cells = n ** 3
     res = {}
-    for d in [int(x) for x in args.depths.split(",") if x]:
+    for d in [int(x) for x in args.depths.split(",") if x and x != "none"]:
         in_s = ctypes.c_int(0)
         iters = max(d, (args.iters // d) * d)
         _lib.check(lib.sb_jacobi(g.data_ptr(), s.data_ptr(), n, n, n, iters, 0.0, 1 / 6, d, sp,
