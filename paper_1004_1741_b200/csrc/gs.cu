@@ -62,7 +62,7 @@ struct GsParams {
     int* ticket;           // atomic task counter
     int* prog;             // [R][ntiles] progress (encoded)
     int* err;              // error word (timeout)
-    const short2* order;   // ticket -> (J, K) within a sweep
+    const int2* order;     // ticket -> (sweep, J | K << 16), in wavefront order
     double* grid;          // the grid (results are written back directly)
 };
 
@@ -76,7 +76,7 @@ struct GsCfg {
     static constexpr int LINES = LJ * LK;
     static constexpr int SLOT = CW * LINES;              // doubles per chunk slot
     static constexpr int SMAX = (BJ - 1) + (BK - 1);     // max line skew
-    static constexpr int R = 4;                          // sweep slots for progress
+    static constexpr int R = 8;                          // sweep slots for progress
     static constexpr int QS = NS + 4;                    // task queue entries (tasks may be
                                                          // as short as one chunk)
     static constexpr uint32_t BOX_BYTES = uint32_t(SLOT) * 8;
@@ -149,10 +149,10 @@ __device__ __forceinline__ GsTask decode_task(const GsParams& p, long long tk) {
         t.J = t.K = t.tile = 0;
         return t;
     }
-    t.s = (int)(tk / p.ntiles);
-    const short2 jk = p.order[tk % p.ntiles];
-    t.J = jk.x;
-    t.K = jk.y;
+    const int2 o = p.order[tk];
+    t.s = o.x;
+    t.J = o.y & 0xffff;
+    t.K = o.y >> 16;
     t.tile = t.K * p.tiles_j + t.J;
     return t;
 }
@@ -406,11 +406,31 @@ struct GsScratch {
     int* words = nullptr;  // ticket, err
     int* prog = nullptr;
     size_t prog_cap = 0;
-    short2* order = nullptr;
+    int2* order = nullptr;
     size_t order_cap = 0;
-    int tj = -1, tk = -1;
+    int tj = -1, tk = -1, ns = -1;
 };
 static GsScratch g_gs[16];
+
+// Ticket order over `sweeps` sweeps of a tiles_j x tiles_k tile grid: by
+// tau = (J + K) + 2 * sweep, then sweep, then J.  Every dependency of task
+// (s, J, K) -- (s, J-1, K), (s, J, K-1) at tau-1, (s-1, J+1, K), (s-1, J, K+1)
+// at tau-1, (s-1, J, K) at tau-2, (s-R+1, J, K) at tau-2(R-1) -- has a smaller
+// ticket, so a persistent grid cannot deadlock, and successive sweeps advance
+// together in a diagonal band instead of one whole wavefront after another.
+static std::vector<int2> wavefront_order(int tiles_j, int tiles_k, int sweeps) {
+    std::vector<int2> ord;
+    ord.reserve(size_t(sweeps) * tiles_j * tiles_k);
+    const int dmax = tiles_j + tiles_k - 2;
+    for (int tau = 0; tau <= dmax + 2 * (sweeps - 1); ++tau)
+        for (int s = std::max(0, (tau - dmax + 1) / 2); s < sweeps && 2 * s <= tau; ++s) {
+            const int d = tau - 2 * s;
+            if (d > dmax) continue;
+            for (int J = std::max(0, d - (tiles_k - 1)); J < tiles_j && J <= d; ++J)
+                ord.push_back(make_int2(s, J | ((d - J) << 16)));
+        }
+    return ord;
+}
 
 template <class C>
 static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double b, bool inter,
@@ -436,26 +456,27 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
         if ((e = cudaMalloc(&S.prog, need * sizeof(int))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
         S.prog_cap = need;
     }
-    if (S.tj != tiles_j || S.tk != tiles_k) {
-        // anti-diagonal order: d = J + K ascending, then J ascending
-        std::vector<short2> ord;
-        ord.reserve(ntiles);
-        for (int d = 0; d <= tiles_j + tiles_k - 2; ++d)
-            for (int J = 0; J < tiles_j; ++J) {
-                const int K = d - J;
-                if (K >= 0 && K < tiles_k) ord.push_back(make_short2((short)J, (short)K));
-            }
-        if (S.order_cap < (size_t)ntiles) {
+    // sweeps per launch: bounded by the order table size and the int32 progress encoding
+    const int64_t nch64 = (ni + 2 + C::CW - 1) / C::CW;
+    const int64_t per_launch = std::max<int64_t>(1, std::min<int64_t>(
+        std::min<int64_t>(512, ((int64_t(1) << 30) / (nch64 + 1)) - 2), (int64_t(1) << 26) / ntiles));
+    const int batch = (int)std::min<int64_t>(iters, per_launch);
+    if (S.tj != tiles_j || S.tk != tiles_k || S.ns != batch) {
+        const std::vector<int2> ord = wavefront_order(tiles_j, tiles_k, batch);
+        if (S.order_cap < ord.size()) {
             if (S.order) cudaFree(S.order);
-            if ((e = cudaMalloc(&S.order, ntiles * sizeof(short2))) != cudaSuccess)
-                return cuda_fail(e, "cudaMalloc");
-            S.order_cap = ntiles;
+            if ((e = cudaMalloc(&S.order, ord.size() * sizeof(int2))) != cudaSuccess)
+                return cuda_fail(e, "cudaMalloc(order)");
+            S.order_cap = ord.size();
         }
-        if ((e = cudaMemcpy(S.order, ord.data(), ntiles * sizeof(short2), cudaMemcpyHostToDevice)) !=
-            cudaSuccess)
+        // stream-ordered: a previous launch on this stream may still read the table
+        if ((e = cudaMemcpyAsync(S.order, ord.data(), ord.size() * sizeof(int2), cudaMemcpyHostToDevice,
+                                 st)) != cudaSuccess)
             return cuda_fail(e, "cudaMemcpy(order)");
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "order upload");
         S.tj = tiles_j;
         S.tk = tiles_k;
+        S.ns = batch;
     }
 
     CUtensorMap lmap, smap;
@@ -488,10 +509,16 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
     p.prog = S.prog;
     p.order = S.order;
     p.grid = grid;
-    // sweeps per launch bounded by the int32 progress encoding
-    const int64_t max_sweeps = ((int64_t(1) << 30) / (p.nch + 1)) - 2;
     for (int64_t done = 0; done < iters;) {
-        const int n = (int)std::min<int64_t>(iters - done, max_sweeps);
+        const int n = (int)std::min<int64_t>(iters - done, batch);
+        if (n != S.ns) {  // a shorter final batch needs its own order table
+            const std::vector<int2> ord = wavefront_order(tiles_j, tiles_k, n);
+            if ((e = cudaMemcpyAsync(S.order, ord.data(), ord.size() * sizeof(int2), cudaMemcpyHostToDevice,
+                                     st)) != cudaSuccess)
+                return cuda_fail(e, "cudaMemcpy(order)");
+            if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "order upload");
+            S.ns = n;
+        }
         p.tasks = (long long)n * ntiles;
         if ((e = cudaMemsetAsync(S.words, 0, 64 * sizeof(int), st)) != cudaSuccess)
             return cuda_fail(e, "memset");
