@@ -63,7 +63,8 @@ struct GsParams {
     int* prog;             // [R][ntiles] progress (encoded)
     int* err;              // error word (timeout)
     const int2* order;     // ticket -> (sweep, J | K << 16), in wavefront order
-    double* grid;          // the grid (results are written back directly)
+    double* grid;          // the grid
+    unsigned long long* prof;  // SB_GS_PROFILE builds: per-CTA cycle counters
 };
 
 template <int BJ_, int BK_, int CW_, int NS_>
@@ -291,80 +292,117 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
     const int nsteps = ni + SMAX;
     uint32_t gc = 0;  // global chunk index of the current task's chunk 0
     int q = 0;
+#ifdef SB_GS_PROFILE
+    unsigned long long w_start = 0, w_chunk = 0, n_tasks = 0;
+    const long long k_t0 = clock64();
+#endif
     while (true) {
+#ifdef SB_GS_PROFILE
+        long long tw = clock64();
+#endif
         if (tid == 0) mbar_wait(&full[gc % NS], (gc / NS) & 1);  // chunk 0 (+ queue entry)
+#ifdef SB_GS_PROFILE
+        w_start += clock64() - tw;
+        ++n_tasks;
+#endif
         named_bar_sync(1, C::NCOMP);
         const GsTask t = queue[q];
         q = (q + 1) % C::QS;
         if (t.s < 0) break;
         const int J0 = 1 + t.J * BJ, K0 = 1 + t.K * C::BK;
         const bool line_in = (J0 + jl <= p.nj) && (K0 + kl <= p.nk);
-        // column i of this line at pi, column i+1 at pe
+        // column i of this line at pi, column i+1 at pe (chunk ce).  The step
+        // loop runs in blocks of CW steps; the CTA-uniform events -- the leading
+        // line entering a new chunk, the trailing line completing one -- fall
+        // on fixed positions of a block.
         int i = 1 - skew;
         double* pi = smem + size_t(gc % NS) * C::SLOT + line * CW + max(i, 0);
         double* pe = pi + 1;
-        int ce = 0;                  // chunk of pe
+        int ce = 0;
+        double* pnext = smem + size_t((gc + 1) % NS) * C::SLOT + line * CW;  // start of chunk ce+1
         double wv = pi[-max(i, 0)];  // column 0: the Dirichlet halo (W of column 1)
-        int ready = 1;       // chunks known loaded (thread 0's view, CTA-wide)
-        int completed = 0;   // chunks completed so far
-        int released = 0;    // chunks handed to the storer (thread 0)
-        for (int st = 0; st < nsteps; ++st, ++i) {
-            if (tid == 0) {  // every thread fenced its writes before the last barrier
-                while (released < completed) mbar_arrive(&done[(gc + released++) % NS]);
-            }
-            if (i >= 1 && i <= ni && line_in) {
-                const double e = *pe;
-                const double sv = pi[-CW], nv = pi[CW];
-                const double dv = pi[-LJ * CW], uv = pi[LJ * CW];
-                double x;
-                if (INTERLEAVED && ni >= 2) {
-                    double tmp = __dadd_rn(e, sv);
-                    tmp = __dadd_rn(tmp, nv);
-                    tmp = __dadd_rn(tmp, dv);
-                    tmp = __dadd_rn(tmp, uv);
-                    x = __dmul_rn(b, __dadd_rn(wv, tmp));
-                } else {
-                    double acc = __dadd_rn(wv, e);
-                    acc = __dadd_rn(acc, sv);
-                    acc = __dadd_rn(acc, nv);
-                    acc = __dadd_rn(acc, dv);
-                    acc = __dadd_rn(acc, uv);
-                    x = __dmul_rn(b, acc);
+        int ready = 1;               // chunks known loaded (thread 0)
+        int completed = 0;           // chunks completed so far
+        int released = 0;            // chunks handed to the storer (thread 0)
+        constexpr int POS_LEAD = CW - 3;                        // (st+3) % CW == 0
+        constexpr int POS_FIN = ((SMAX - 2) % CW + CW) % CW;    // (st+2-SMAX) % CW == 0
+        for (int st0 = 0; st0 < nsteps; st0 += CW) {
+#pragma unroll
+            for (int pos = 0; pos < CW; ++pos, ++i) {
+                const int st = st0 + pos;
+                if (tid == 0) {  // every thread fenced its writes before the last barrier
+                    while (released < completed) mbar_arrive(&done[(gc + released++) % NS]);
                 }
-                *pi = x;
-                wv = x;
-            }
-            if (i >= 0) {  // advance: pi to column i+1, pe to column i+2
-                pi = pe;
-                if ((i + 2) % CW == 0 && i + 2 < nch * CW) {
-                    ++ce;
-                    pe = smem + size_t((gc + ce) % NS) * C::SLOT + line * CW;
-                } else {
-                    ++pe;
+                {
+                    const double e = *pe;
+                    const double sv = pi[-CW], nv = pi[CW];
+                    const double dv = pi[-LJ * CW], uv = pi[LJ * CW];
+                    double x;
+                    if (INTERLEAVED) {
+                        double tmp = __dadd_rn(e, sv);
+                        tmp = __dadd_rn(tmp, nv);
+                        tmp = __dadd_rn(tmp, dv);
+                        tmp = __dadd_rn(tmp, uv);
+                        x = __dmul_rn(b, __dadd_rn(wv, tmp));
+                    } else {
+                        double acc = __dadd_rn(wv, e);
+                        acc = __dadd_rn(acc, sv);
+                        acc = __dadd_rn(acc, nv);
+                        acc = __dadd_rn(acc, dv);
+                        acc = __dadd_rn(acc, uv);
+                        x = __dmul_rn(b, acc);
+                    }
+                    const bool active = line_in && (i >= 1) && (i <= ni);
+                    if (active) *pi = x;
+                    wv = active ? x : wv;
                 }
-            }
-            // trailing line (skew SMAX) just finished column st+1-SMAX: chunks
-            // below that are complete; the last step completes everything
-            const int fin = (st == nsteps - 1) ? nch : min(nch, max(0, (st + 2 - SMAX) / CW));
-            if (fin > completed) {
-                fence_proxy_async_smem();  // this thread's smem writes -> async proxy
-                completed = fin;           // released after this step's barrier
-            }
-            // the leading line (skew 0) reads column st+3 next step
-            if (tid == 0) {
-                const int cneed = (st + 3) / CW;
-                if (cneed < nch && cneed >= ready) {
-                    mbar_wait(&full[(gc + cneed) % NS], ((gc + cneed) / NS) & 1);
-                    ready = cneed + 1;
+                if (i >= 0) {  // advance: pi to column i+1, pe to column i+2
+                    pi = pe;
+                    if (((i + 2) & (CW - 1)) == 0) {
+                        ++ce;
+                        pe = pnext;
+                        pnext = smem + size_t((gc + ce + 1) % NS) * C::SLOT + line * CW;
+                    } else {
+                        ++pe;
+                    }
                 }
+                if (pos == POS_FIN || st == nsteps - 1) {
+                    const int fin = (st >= nsteps - 1) ? nch : min(nch, max(0, (st + 2 - SMAX) / CW));
+                    if (fin > completed) {
+                        fence_proxy_async_smem();  // this thread's smem writes -> async proxy
+                        completed = fin;           // released after this step's barrier
+                    }
+                }
+                if (pos == POS_LEAD && tid == 0) {  // the leading line reads column st+3 next step
+                    const int cneed = (st + 3) / CW;
+                    if (cneed < nch && cneed >= ready) {
+#ifdef SB_GS_PROFILE
+                        long long tc = clock64();
+#endif
+                        mbar_wait(&full[(gc + cneed) % NS], ((gc + cneed) / NS) & 1);
+#ifdef SB_GS_PROFILE
+                        w_chunk += clock64() - tc;
+#endif
+                        ready = cneed + 1;
+                    }
+                }
+                named_bar_sync(1, C::NCOMP);
+                if (st == nsteps - 1) break;
             }
-            named_bar_sync(1, C::NCOMP);
         }
         if (tid == 0) {
             while (released < completed) mbar_arrive(&done[(gc + released++) % NS]);
         }
         gc += nch;
     }
+#ifdef SB_GS_PROFILE
+    if (tid == 0 && p.prof) {
+        atomicAdd(&p.prof[0], (unsigned long long)(clock64() - k_t0));
+        atomicAdd(&p.prof[1], w_start);
+        atomicAdd(&p.prof[2], w_chunk);
+        atomicAdd(&p.prof[3], n_tasks);
+    }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -411,6 +449,13 @@ struct GsScratch {
     int tj = -1, tk = -1, ns = -1;
 };
 static GsScratch g_gs[16];
+#ifdef SB_GS_PROFILE
+static unsigned long long* g_gs_prof = nullptr;
+extern "C" void sb_gs_profile(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    if (g_gs_prof) cudaMemcpy(out, g_gs_prof, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+}
+#endif
 
 // Ticket order over `sweeps` sweeps of a tiles_j x tiles_k tile grid: by
 // tau = (J + K) + 2 * sweep, then sweep, then J.  Every dependency of task
@@ -509,6 +554,14 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
     p.prog = S.prog;
     p.order = S.order;
     p.grid = grid;
+    p.prof = nullptr;
+#ifdef SB_GS_PROFILE
+    static unsigned long long* prof = nullptr;
+    if (!prof) cudaMalloc(&prof, 64);
+    cudaMemsetAsync(prof, 0, 64, st);
+    p.prof = prof;
+    g_gs_prof = prof;
+#endif
     for (int64_t done = 0; done < iters;) {
         const int n = (int)std::min<int64_t>(iters - done, batch);
         if (n != S.ns) {  // a shorter final batch needs its own order table

@@ -1,0 +1,16 @@
+"""Dev: GS wait-time breakdown with the SB_GS_PROFILE build."""
+import ctypes, sys
+from pathlib import Path
+import torch
+lib = ctypes.CDLL(str(Path(__file__).resolve().parent / "libsb200_prof.so"))
+lib.sb_gs.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_int, ctypes.c_void_p]
+lib.sb_gs_profile.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+for (n, nj, nk, it) in [(512, 16, 16, 4), (512, 512, 16, 2), (512, 512, 512, 16)]:
+    g = torch.rand((nk + 2, nj + 2, n + 2), dtype=torch.float64, device="cuda")
+    lib.sb_gs(g.data_ptr(), n, nj, nk, 1, 1/6, 1, None); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); rc = lib.sb_gs(g.data_ptr(), n, nj, nk, it, 1/6, 1, None); e1.record(); torch.cuda.synchronize()
+    out = (ctypes.c_ulonglong * 4)(); lib.sb_gs_profile(out)
+    tot, ws, wc, nt = list(out)
+    print(f"{n}x{nj}x{nk}x{it}: {e0.elapsed_time(e1):.3f} ms rc={rc}; per-CTA cycles total {tot/148:.3g}; "
+          f"wait task-start {100*ws/tot:.1f}%, wait chunk {100*wc/tot:.1f}%, tasks {nt}", flush=True)
