@@ -41,6 +41,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdint>
 #include <vector>
 
@@ -326,19 +327,24 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
         int released = 0;            // chunks handed to the storer (thread 0)
         constexpr int POS_LEAD = CW - 3;                        // (st+3) % CW == 0
         constexpr int POS_FIN = ((SMAX - 2) % CW + CW) % CW;    // (st+2-SMAX) % CW == 0
-        for (int st0 = 0; st0 < nsteps; st0 += CW) {
+        // One block of CW plane steps.  FULL: every line computes at every step
+        // of the block (no prologue/epilogue of the skew, no partial tile).
+        auto block = [&](const int st0, auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
             for (int pos = 0; pos < CW; ++pos, ++i) {
                 const int st = st0 + pos;
-                if (tid == 0) {  // every thread fenced its writes before the last barrier
-                    while (released < completed) mbar_arrive(&done[(gc + released++) % NS]);
+                if (pos == POS_FIN + 1 || pos == 0) {  // every thread fenced before the last barrier
+                    if (tid == 0)
+                        while (released < completed) mbar_arrive(&done[(gc + released++) % NS]);
                 }
-                {
+                const bool active = FULL || (line_in && (i >= 1) && (i <= ni));
+                if (active) {
                     const double e = *pe;
                     const double sv = pi[-CW], nv = pi[CW];
                     const double dv = pi[-LJ * CW], uv = pi[LJ * CW];
                     double x;
-                    if (INTERLEAVED) {
+                    if (INTERLEAVED) {  // (ni >= 2 on this path: ni+2 is even)
                         double tmp = __dadd_rn(e, sv);
                         tmp = __dadd_rn(tmp, nv);
                         tmp = __dadd_rn(tmp, dv);
@@ -352,11 +358,10 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
                         acc = __dadd_rn(acc, uv);
                         x = __dmul_rn(b, acc);
                     }
-                    const bool active = line_in && (i >= 1) && (i <= ni);
-                    if (active) *pi = x;
-                    wv = active ? x : wv;
+                    *pi = x;
+                    wv = x;
                 }
-                if (i >= 0) {  // advance: pi to column i+1, pe to column i+2
+                if (FULL || i >= 0) {  // advance: pi to column i+1, pe to column i+2
                     pi = pe;
                     if (((i + 2) & (CW - 1)) == 0) {
                         ++ce;
@@ -366,7 +371,7 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
                         ++pe;
                     }
                 }
-                if (pos == POS_FIN || st == nsteps - 1) {
+                if (pos == POS_FIN || (!FULL && st == nsteps - 1)) {
                     const int fin = (st >= nsteps - 1) ? nch : min(nch, max(0, (st + 2 - SMAX) / CW));
                     if (fin > completed) {
                         fence_proxy_async_smem();  // this thread's smem writes -> async proxy
@@ -387,8 +392,17 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
                     }
                 }
                 named_bar_sync(1, C::NCOMP);
-                if (st == nsteps - 1) break;
+                if (!FULL && st == nsteps - 1) break;
             }
+        };
+        // full blocks: the trailing line (skew SMAX) is at column >= 1 at the
+        // block's first step and the leading line at column <= ni at its last
+        const bool tile_full = (J0 + C::BJ - 1 <= p.nj) && (K0 + C::BK - 1 <= p.nk);
+        for (int st0 = 0; st0 < nsteps; st0 += CW) {
+            if (tile_full && st0 + 1 - SMAX >= 1 && st0 + CW <= ni && st0 + CW < nsteps)
+                block(st0, std::true_type{});
+            else
+                block(st0, std::false_type{});
         }
         if (tid == 0) {
             while (released < completed) mbar_arrive(&done[(gc + released++) % NS]);
