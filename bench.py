@@ -343,7 +343,7 @@ def run_gpu_arm(args):
     also = {}
     if world == 1 and not args.no_also:
         n5 = 512
-        also["cfg3_jacobi512_depths"] = time_jacobi_depths(torch, lib, n5, 96, [1, 2, 4, 8])
+        also["cfg3_jacobi512_depths"] = time_jacobi_depths(torch, lib, n5, 100, [1, 2, 3, 4, 8])
         also["cfg5_gs512_naive"] = time_gs(torch, lib, n5, args.gs_sweeps, 1)
         also["cfg5_gs512_interleaved"] = time_gs(torch, lib, n5, args.gs_sweeps, 2)
 
@@ -396,8 +396,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--depth", type=int, default=4)
-    ap.add_argument("--gs-sweeps", type=int, default=20)
+    ap.add_argument("--depth", type=int, default=3)
+    ap.add_argument("--gs-sweeps", type=int, default=100)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-also", action="store_true")

@@ -100,7 +100,8 @@ int sb_jacobi(double* grid, double* scratch, int64_t ni, int64_t nj, int64_t nk,
  * Lexicographic Gauss-Seidel sweeps, in place on the device grid.
  * kernel: SB_KERNEL_GS_NAIVE or SB_KERNEL_GS_INTERLEAVED (selects the
  * association, bitwise equal to the matching reference kernel).
- * Asynchronous on `stream`.
+ * Asynchronous on `stream`.  GS calls on one device share its scheduling
+ * state: issue them on one stream (or synchronise between streams).
  */
 int sb_gs(double* grid, int64_t ni, int64_t nj, int64_t nk, int64_t iters, double b,
           int kernel, void* stream);

@@ -87,9 +87,14 @@ int make_grid_map(CUtensorMap* m, const double* base, int64_t nip, int64_t njp, 
 
 // ---------------------------------------------------------------------------
 // per-device context: SM count, work counters
+// Work counters: every launch takes its own slot from a rotating pool, so
+// kernels running concurrently on different streams of one device (z-slabs
+// sharing a GPU) never share a counter.
+constexpr int kCounterSlots = 4096;
 struct DevCtx {
     int sms = 0;
-    int* counters = nullptr;  // device ints
+    int* counters = nullptr;  // device ints, kCounterSlots of them
+    unsigned seq = 0;         // next slot
 };
 static std::mutex g_ctx_mu;
 static std::vector<DevCtx> g_ctx;
@@ -104,7 +109,7 @@ int dev_ctx(DevCtx** out) {
     if (!c.counters) {
         e = cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
         if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
-        e = cudaMalloc(&c.counters, 64 * sizeof(int));
+        e = cudaMalloc(&c.counters, kCounterSlots * sizeof(int));
         if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(counters)");
     }
     *out = &c;
@@ -115,7 +120,8 @@ int get_counters(int** counters, int* sms) {
     DevCtx* c;
     int rc = dev_ctx(&c);
     if (rc) return rc;
-    *counters = c->counters;
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    *counters = c->counters + (c->seq++ % kCounterSlots);
     *sms = c->sms;
     return SB_OK;
 }

@@ -1,0 +1,137 @@
+"""z-slab decomposition (multi-GPU Jacobi): the exchange logic of
+paper_1004_1741_b200.slabs on CPU with gloo (world size 2, oracle compute),
+and on one GPU with several slabs (C ABI sb_jacobi_slabs and SlabEngine)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import make_input, sha
+
+from paper_1004_1741_b200.slabs import slab_layout
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def cpu_compute(a, b):
+    """Oracle stand-in for sb_jacobi_planes: T sweeps of the local grid,
+    keep only the output planes (test infrastructure)."""
+    import torch
+
+    def compute(src, dst, nkl, k_lo, k_hi, sweeps):
+        if k_hi <= k_lo:
+            return
+        out = oracle.run_serial("jacobi", src.numpy(), sweeps, a, b)
+        dst[k_lo:k_hi] = torch.from_numpy(out[k_lo:k_hi])
+
+    return compute
+
+
+def _gloo_worker(rank, world, port, spec, iters, depth, a, b, result_path):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1004_1741_b200.slabs import SlabEngine
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = make_input(spec)
+    eng = SlabEngine(g.ni, g.nj, g.nk, depth, rank, world, cpu_compute(a, b),
+                     like=torch.empty(0, dtype=torch.float64))
+    eng.load_global(g.data)
+    eng.run(iters)
+    owned = eng.owned().contiguous()
+    if rank == 0:
+        parts = [owned]
+        for r in range(1, world):
+            lo, hi, _, _ = slab_layout(g.nk, world, r, depth)
+            t = torch.empty((hi - lo, g.nj + 2, g.ni + 2), dtype=torch.float64)
+            dist.recv(t, src=r)
+            parts.append(t)
+        np.save(result_path, torch.cat(parts).numpy())
+    else:
+        dist.send(owned, dst=0)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shape,iters,depth,coeffs", [
+    ((12, 10, 16), 7, 2, (0.0, 1 / 6)),
+    ((9, 8, 13), 5, 3, (0.5, 0.1)),
+    ((6, 6, 4), 4, 1, (0.5, 0.1)),
+])
+def test_gloo_two_ranks_bitwise_equal_single_grid(tmp_path, shape, iters, depth, coeffs):
+    import torch.multiprocessing as mp
+
+    spec = {"shape": list(shape), "pattern": "random", "seed": 5, "lo": -1.0, "hi": 1.0}
+    out = tmp_path / "owned.npy"
+    mp.start_processes(_gloo_worker, args=(2, _free_port(), spec, iters, depth, *coeffs, str(out)),
+                       nprocs=2, join=True, start_method="spawn")
+    got = np.load(out)
+    want = oracle.run_serial("jacobi", make_input(spec).data, iters, *coeffs)[1:-1]
+    assert sha(got) == sha(want)
+
+
+def test_slab_layout_ghosts():
+    assert slab_layout(10, 1, 0, 4) == (1, 11, 1, 1)
+    assert slab_layout(10, 3, 1, 2) == (5, 8, 2, 2)
+    assert slab_layout(10, 3, 0, 2)[2] == 1 and slab_layout(10, 3, 2, 2)[3] == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nslabs,depth,iters", [(2, 2, 7), (3, 4, 9), (4, 1, 5), (2, 8, 16)])
+def test_c_abi_slabs_on_one_gpu(nslabs, depth, iters):
+    import ctypes
+
+    import torch
+
+    from paper_1004_1741_b200 import _lib
+
+    lib = _lib.load()
+    spec = {"shape": [64, 30, 40], "pattern": "random", "seed": 9, "lo": 0.0, "hi": 1.0}
+    g = make_input(spec)
+    want = oracle.run_serial("jacobi", g.data, iters, 0.0, 1 / 6)
+    bufs, scr = [], []
+    for s in range(nslabs):
+        lo, hi, gl, gh = slab_layout(g.nk, nslabs, s, depth)
+        part = torch.from_numpy(np.ascontiguousarray(g.data[lo - gl:hi + gh])).cuda()
+        bufs.append(part)
+        scr.append(torch.empty_like(part))
+    devs = (ctypes.c_int * nslabs)(*([0] * nslabs))
+    pa = (ctypes.c_void_p * nslabs)(*[t.data_ptr() for t in bufs])
+    pb = (ctypes.c_void_p * nslabs)(*[t.data_ptr() for t in scr])
+    streams = [torch.cuda.Stream() for _ in range(nslabs)]
+    ps = (ctypes.c_void_p * nslabs)(*[s.cuda_stream for s in streams])
+    res = ctypes.c_int(-1)
+    _lib.check(lib.sb_jacobi_slabs(nslabs, devs, pa, pb, g.ni, g.nj, g.nk, iters, 0.0, 1 / 6, depth,
+                                   ps, ctypes.byref(res)))
+    owned = []
+    for s in range(nslabs):
+        lo, hi, gl, gh = slab_layout(g.nk, nslabs, s, depth)
+        t = (scr if res.value else bufs)[s]
+        owned.append(t[gl:gl + hi - lo].cpu().numpy())
+    assert sha(np.concatenate(owned)) == sha(want[1:-1])
+
+
+@pytest.mark.gpu
+def test_slab_engine_single_rank_matches_oracle():
+    import torch
+
+    from paper_1004_1741_b200.slabs import SlabEngine, gpu_compute
+
+    spec = {"shape": [62, 20, 33], "pattern": "random", "seed": 4, "lo": 0.0, "hi": 1.0}
+    g = make_input(spec)
+    eng = SlabEngine(g.ni, g.nj, g.nk, 4, 0, 1, gpu_compute(g.ni, g.nj, 0.0, 1 / 6),
+                     like=torch.empty(0, dtype=torch.float64, device="cuda"))
+    eng.load_global(g.data)
+    eng.run(10)
+    torch.cuda.synchronize()
+    want = oracle.run_serial("jacobi", g.data, 10, 0.0, 1 / 6)
+    assert sha(eng.owned().cpu().numpy()) == sha(want[1:-1])
