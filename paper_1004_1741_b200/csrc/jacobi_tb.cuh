@@ -282,22 +282,31 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
     return ++s.n == it.N;
 }
 
-// All plane steps of one item, entering the 3-phase rotation at g mod 3.
+// `count` plane steps of the current item (all of them FAST or not),
+// entering the 3-phase register rotation at g mod 3.
 template <class C, bool FAST, bool AZ>
-__device__ __forceinline__ void jacobi_item(const CUtensorMap* src_map, const JacobiParams& p,
-                                         double* ring, double* xb, uint64_t* full, ItemInfo* queue,
-                                         LevelQ<C> (&Q)[C::T], JState& s) {
+__device__ __forceinline__ void jacobi_steps(const CUtensorMap* src_map, const JacobiParams& p,
+                                             double* ring, double* xb, uint64_t* full,
+                                             ItemInfo* queue, LevelQ<C> (&Q)[C::T], JState& s,
+                                             int count) {
+    if (count <= 0) return;
     const int ph = s.g % 3;
     if (ph == 1) {
-        if (jacobi_step<C, FAST, AZ, 1>(src_map, p, ring, xb, full, queue, Q, s)) return;
-        if (jacobi_step<C, FAST, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s)) return;
+        jacobi_step<C, FAST, AZ, 1>(src_map, p, ring, xb, full, queue, Q, s);
+        if (--count == 0) return;
+        jacobi_step<C, FAST, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s);
+        if (--count == 0) return;
     } else if (ph == 2) {
-        if (jacobi_step<C, FAST, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s)) return;
+        jacobi_step<C, FAST, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s);
+        if (--count == 0) return;
     }
     while (true) {
-        if (jacobi_step<C, FAST, AZ, 0>(src_map, p, ring, xb, full, queue, Q, s)) return;
-        if (jacobi_step<C, FAST, AZ, 1>(src_map, p, ring, xb, full, queue, Q, s)) return;
-        if (jacobi_step<C, FAST, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s)) return;
+        jacobi_step<C, FAST, AZ, 0>(src_map, p, ring, xb, full, queue, Q, s);
+        if (--count == 0) return;
+        jacobi_step<C, FAST, AZ, 1>(src_map, p, ring, xb, full, queue, Q, s);
+        if (--count == 0) return;
+        jacobi_step<C, FAST, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s);
+        if (--count == 0) return;
     }
 }
 
@@ -339,15 +348,18 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map, const JacobiParams
     s.cq = 0;
     s.it = queue[0];
     while (s.it.N > 0) {
-        // FAST when every cell computed for this item is interior: the input
-        // box (less its 1-cell rim) lies inside [1,ni] x [1,nj] for all planes
-        // [kb-T+1, ke+T-1)
-        const int ke = s.it.kb + s.it.N - 2 * T;
-        const bool fast = (s.it.I0 - C::H >= 1) && (s.it.I0 - C::H + C::BW - 1 <= p.ni) &&
-                          (s.it.J0 - (T - 1) >= 1) && (s.it.J0 - (T - 1) + C::ROWS - 1 <= p.nj) &&
-                          (s.it.kb - T + 1 >= 1) && (ke + T - 2 <= p.nk);
-        if (fast) jacobi_item<C, true, AZ>(&src_map, p, ring, xb, full, queue, Q, s);
-        else jacobi_item<C, false, AZ>(&src_map, p, ring, xb, full, queue, Q, s);
+        // FAST steps: every cell computed is interior -- the tile's rows and
+        // columns lie inside [1,nj] x [1,ni] (per item) and all T planes the
+        // levels compute at this step lie inside [1,nk] (per step: only the
+        // first/last steps of items touching the k boundary are excluded)
+        const bool ij_in = (s.it.I0 - C::H >= 1) && (s.it.I0 - C::H + C::BW - 1 <= p.ni) &&
+                           (s.it.J0 - (T - 1) >= 1) && (s.it.J0 - (T - 1) + C::ROWS - 1 <= p.nj);
+        // step n computes planes kb-T+n-L for L = 1..T
+        const int n_lo = ij_in ? min(s.it.N, max(0, 2 * T + 1 - s.it.kb)) : s.it.N;
+        const int n_hi = ij_in ? max(n_lo, min(s.it.N, p.nk + 2 + T - s.it.kb)) : s.it.N;
+        jacobi_steps<C, false, AZ>(&src_map, p, ring, xb, full, queue, Q, s, n_lo);
+        jacobi_steps<C, true, AZ>(&src_map, p, ring, xb, full, queue, Q, s, n_hi - n_lo);
+        jacobi_steps<C, false, AZ>(&src_map, p, ring, xb, full, queue, Q, s, s.it.N - n_hi);
         s.n = 0;
         __syncthreads();  // queue[] entry written by thread 0 at least one barrier ago
         s.cq = (s.cq + 1) % C::QSLOTS;

@@ -272,9 +272,8 @@ static int launch_depth(int T, const double* src, double* dst, int ni, int nj, i
             if (v == 1) SB_L(3, 4, 8, 4, 1);
             SB_L(3, 2, 16, 4, 1);
         case 4:
-            if (v == 1) SB_L(4, 4, 8, 4, 1);
-            if (v == 2) SB_L(4, 2, 16, 3, 1);
-            SB_L(4, 2, 16, 4, 1);
+            if (v == 1) SB_L(4, 2, 16, 4, 1);
+            SB_L(4, 4, 8, 4, 1);
         case 5: SB_L(5, 2, 12, 3, 1);
         case 6: SB_L(6, 2, 12, 3, 1);
         case 7: SB_L(7, 2, 12, 3, 1);
