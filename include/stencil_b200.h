@@ -115,6 +115,26 @@ int sb_gs(double* grid, int64_t ni, int64_t nj, int64_t nk, int64_t iters, doubl
 int sb_sync(void* stream);
 
 /*
+ * The library's plain "serial engine": straightforward kernels without
+ * tiling or temporal blocking (one sweep per launch for Jacobi, a single
+ * thread in exact lexicographic order for GS).  Used by the CLI's verify to
+ * check the optimised paths, as the reference's verify checks its variants
+ * against run_serial (cli.py:297-331).  Slow by design.  Jacobi ping-pongs
+ * grid/scratch like sb_jacobi; GS ignores scratch and a.  Asynchronous.
+ */
+int sb_reference_sweeps(int kernel, double* grid, double* scratch, int64_t ni, int64_t nj,
+                        int64_t nk, int64_t iters, double a, double b, void* stream,
+                        int* result_in_scratch);
+
+/*
+ * Line-level update (reference kernels.py:212-247): interior line (k, j).
+ * Jacobi writes dst from src (distinct buffers); GS updates src in place
+ * (dst ignored).  Bounds are checked (SB_ERR_ARGUMENT).  Asynchronous.
+ */
+int sb_line_update(int kernel, const double* src, double* dst, int64_t ni, int64_t nj,
+                   int64_t nk, int64_t k, int64_t j, double a, double b, void* stream);
+
+/*
  * Host-buffer entry point: the whole reference `run` contract in one call.
  * host_grid: padded grid in host memory (pinned or pageable), updated in
  * place with the final field.  Copies to device `device`, sweeps, copies
@@ -123,6 +143,14 @@ int sb_sync(void* stream);
  */
 int sb_run_host(int kernel, double* host_grid, int64_t ni, int64_t nj, int64_t nk,
                 int64_t iters, double a, double b, int depth, int device);
+
+/*
+ * Device bandwidth probe: a[i] = b[i] + s*c[i] for n doubles (device
+ * pointers, 16-byte aligned), the STREAM triad of the reference's
+ * perf.stream_triad (pkg/src/stencilbench/perf.py:139-211) on the GPU.
+ * 24 bytes per element move.  Asynchronous on `stream`.
+ */
+int sb_triad(double* a, const double* b, const double* c, double s, int64_t n, void* stream);
 
 /*
  * Pinned host allocation for grids (so sb_run_host copies at full PCIe

@@ -40,7 +40,11 @@ SIGNATURES = {
                          ctypes.POINTER(_int)]),
     "sb_gs": (_int, [_vp, _i64, _i64, _i64, _i64, _dbl, _int, _vp]),
     "sb_sync": (_int, [_vp]),
+    "sb_line_update": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _dbl, _dbl, _vp]),
+    "sb_reference_sweeps": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _dbl, _dbl, _vp,
+                                   ctypes.POINTER(_int)]),
     "sb_run_host": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _dbl, _dbl, _int, _int]),
+    "sb_triad": (_int, [_vp, _vp, _vp, _dbl, _i64, _vp]),
     "sb_host_alloc": (_vp, [_i64]),
     "sb_host_free": (None, [_vp]),
     "sb_jacobi_planes": (_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _int, _dbl, _dbl, _vp]),

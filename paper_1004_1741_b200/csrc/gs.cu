@@ -42,6 +42,7 @@
 
 #include <algorithm>
 #include <type_traits>
+#include <utility>
 #include <cstdint>
 #include <vector>
 
@@ -600,20 +601,26 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
     return SB_OK;
 }
 
+int gs_serial_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,
+                  cudaStream_t st);
+
 int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,
            cudaStream_t st) {
+    if (!tma_ok(grid, ni)) return gs_serial_run(grid, ni, nj, nk, iters, b, kernel, st);
+    return gs_launch<GsC>(grid, ni, nj, nk, iters, b, kernel == SB_KERNEL_GS_INTERLEAVED, st);
+}
+
+int gs_serial_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,
+                  cudaStream_t st) {
     const bool inter = (kernel == SB_KERNEL_GS_INTERLEAVED);
-    if (!tma_ok(grid, ni)) {
-        for (int64_t done = 0; done < iters;) {
-            const int n = (int)std::min<int64_t>(iters - done, 1 << 20);
-            if (inter) gs_serial_kernel<true><<<1, 32, 0, st>>>(grid, ni, nj, nk, n, b);
-            else gs_serial_kernel<false><<<1, 32, 0, st>>>(grid, ni, nj, nk, n, b);
-            done += n;
-        }
-        cudaError_t e = cudaGetLastError();
-        return e == cudaSuccess ? SB_OK : cuda_fail(e, "gs_serial launch");
+    for (int64_t done = 0; done < iters;) {
+        const int n = (int)std::min<int64_t>(iters - done, 1 << 20);
+        if (inter) gs_serial_kernel<true><<<1, 32, 0, st>>>(grid, ni, nj, nk, n, b);
+        else gs_serial_kernel<false><<<1, 32, 0, st>>>(grid, ni, nj, nk, n, b);
+        done += n;
     }
-    return gs_launch<GsC>(grid, ni, nj, nk, iters, b, inter, st);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SB_OK : cuda_fail(e, "gs_serial launch");
 }
 
 // error word readback (host) -- called by the synchronous entry points
@@ -652,4 +659,98 @@ extern "C" int sb_sync(void* stream) {
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "stream synchronize");
     return gs_check_error(st);
+}
+
+// The library's "serial engine": straightforward kernels with none of the
+// tiling, pipelining or temporal blocking -- one plain sweep per launch for
+// Jacobi, a single thread in exact lexicographic order for GS.  The CLI's
+// verify compares the optimised paths against it (reference cli.py:297-331
+// compares its parallel variants against run_serial the same way).
+extern "C" int sb_reference_sweeps(int kernel, double* grid, double* scratch, int64_t ni, int64_t nj,
+                                   int64_t nk, int64_t iters, double a, double b, void* stream,
+                                   int* result_in_scratch) {
+    using namespace sb;
+    clear_error();
+    int rc = check_dims(ni, nj, nk);
+    if (rc) return rc;
+    if (iters < 0) return fail(SB_ERR_PLAN, "iter_end must be >= 0, got %lld", (long long)iters);
+    if (!grid || !result_in_scratch) return fail(SB_ERR_ARGUMENT, "null pointer");
+    *result_in_scratch = 0;
+    if (iters == 0) return SB_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (kernel == SB_KERNEL_JACOBI) {
+        if (!scratch || scratch == grid) return fail(SB_ERR_ARGUMENT, "Jacobi needs a distinct scratch grid");
+        if ((rc = halo_copy(grid, scratch, (int)ni, (int)nj, (int)nk, st))) return rc;
+        double* src = grid;
+        double* dst = scratch;
+        for (int64_t s = 0; s < iters; ++s) {
+            if ((rc = jacobi_generic_sweep(src, dst, (int)ni, (int)nj, (int)nk, a, b, st))) return rc;
+            std::swap(src, dst);
+        }
+        *result_in_scratch = (src == scratch);
+        return SB_OK;
+    }
+    if (kernel != SB_KERNEL_GS_NAIVE && kernel != SB_KERNEL_GS_INTERLEAVED)
+        return fail(SB_ERR_PLAN, "unknown kernel %d", kernel);
+    return gs_serial_run(grid, (int)ni, (int)nj, (int)nk, iters, b, kernel, st);
+}
+
+// One line update (reference kernels.py:212-247): interior line (k, j) --
+// Jacobi out of place (src -> dst, the i loop is parallel), GS in place on
+// `src` (sequential along i, one thread).
+__global__ void line_kernel(int kernel, const double* src, double* dst, int ni, int nj, int k, int j,
+                            double a, double b) {
+    const int64_t nip = ni + 2, plane = nip * (nj + 2);
+    const int64_t base = (int64_t)(k + 1) * plane + (int64_t)(j + 1) * nip;
+    if (kernel == SB_KERNEL_JACOBI) {
+        for (int i = 1 + threadIdx.x; i <= ni; i += blockDim.x) {
+            const double* c = src + base + i;
+            double acc = __dadd_rn(c[-1], c[1]);
+            acc = __dadd_rn(acc, c[-nip]);
+            acc = __dadd_rn(acc, c[nip]);
+            acc = __dadd_rn(acc, c[-plane]);
+            acc = __dadd_rn(acc, c[plane]);
+            dst[base + i] = __dadd_rn(__dmul_rn(a, c[0]), __dmul_rn(b, acc));
+        }
+        return;
+    }
+    if (threadIdx.x != 0) return;
+    double* c = const_cast<double*>(src) + base;
+    if (kernel == SB_KERNEL_GS_INTERLEAVED && ni >= 2) {
+        for (int i = 1; i <= ni; ++i) {
+            double tmp = __dadd_rn(c[i + 1], c[i - nip]);
+            tmp = __dadd_rn(tmp, c[i + nip]);
+            tmp = __dadd_rn(tmp, c[i - plane]);
+            tmp = __dadd_rn(tmp, c[i + plane]);
+            c[i] = __dmul_rn(b, __dadd_rn(c[i - 1], tmp));
+        }
+    } else {
+        for (int i = 1; i <= ni; ++i) {
+            double acc = __dadd_rn(c[i - 1], c[i + 1]);
+            acc = __dadd_rn(acc, c[i - nip]);
+            acc = __dadd_rn(acc, c[i + nip]);
+            acc = __dadd_rn(acc, c[i - plane]);
+            acc = __dadd_rn(acc, c[i + plane]);
+            c[i] = __dmul_rn(b, acc);
+        }
+    }
+}
+
+extern "C" int sb_line_update(int kernel, const double* src, double* dst, int64_t ni, int64_t nj,
+                              int64_t nk, int64_t k, int64_t j, double a, double b, void* stream) {
+    using namespace sb;
+    clear_error();
+    int rc = check_dims(ni, nj, nk);
+    if (rc) return rc;
+    if (kernel < SB_KERNEL_JACOBI || kernel > SB_KERNEL_GS_INTERLEAVED)
+        return fail(SB_ERR_PLAN, "unknown kernel %d", kernel);
+    if (k < 0 || k >= nk || j < 0 || j >= nj)
+        return fail(SB_ERR_ARGUMENT, "line (k=%lld, j=%lld) outside interior of %lldx%lld planes",
+                    (long long)k, (long long)j, (long long)nk, (long long)nj);
+    if (!src || (kernel == SB_KERNEL_JACOBI && (!dst || dst == src)))
+        return fail(SB_ERR_ARGUMENT, "Jacobi needs distinct src and dst");
+    line_kernel<<<1, kernel == SB_KERNEL_JACOBI ? 256 : 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        kernel, src, dst, (int)ni, (int)nj, (int)k, (int)j, a, b);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SB_OK : cuda_fail(e, "line kernel launch");
 }

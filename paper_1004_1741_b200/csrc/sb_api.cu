@@ -182,6 +182,22 @@ __global__ void jacobi_generic_kernel(const double* __restrict__ src, double* __
     }
 }
 
+// STREAM-style triad a[i] = b[i] + s*c[i] (reference perf.py:45-48, the
+// bandwidth probe behind predict_p0): 16-byte vector accesses, grid-stride,
+// no contraction (bitwise equal to the numpy check of the reference).
+__global__ void triad_kernel(double* __restrict__ a, const double* __restrict__ b,
+                             const double* __restrict__ c, double s, int64_t n) {
+    const int64_t n2 = n / 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n2; t += stride) {
+        const double2 x = reinterpret_cast<const double2*>(b)[t];
+        const double2 y = reinterpret_cast<const double2*>(c)[t];
+        reinterpret_cast<double2*>(a)[t] =
+            make_double2(__dadd_rn(x.x, __dmul_rn(s, y.x)), __dadd_rn(x.y, __dmul_rn(s, y.y)));
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) a[n - 1] = __dadd_rn(b[n - 1], __dmul_rn(s, c[n - 1]));
+}
+
 // ---------------------------------------------------------------------------
 // temporally blocked launch
 
@@ -294,6 +310,11 @@ static int launch_generic(const double* src, double* dst, int ni, int nj, int kf
     return e == cudaSuccess ? SB_OK : cuda_fail(e, "jacobi_generic launch");
 }
 
+int jacobi_generic_sweep(const double* src, double* dst, int ni, int nj, int nk, double a, double b,
+                         cudaStream_t st) {
+    return launch_generic(src, dst, ni, nj, 1, nk + 1, a, b, st);
+}
+
 int check_dims(int64_t ni, int64_t nj, int64_t nk) {
     if (ni < 1 || nj < 1 || nk < 1)
         return fail(SB_ERR_DIMENSION, "extents must be positive, got %lldx%lldx%lld",
@@ -387,6 +408,22 @@ int sb_jacobi(double* grid, double* scratch, int64_t ni, int64_t nj, int64_t nk,
     if ((rc = halo_copy(grid, scratch, (int)ni, (int)nj, (int)nk, st))) return rc;
     return jacobi_run(grid, scratch, (int)ni, (int)nj, (int)nk, iters, a, b, depth, st,
                       result_in_scratch);
+}
+
+int sb_triad(double* a, const double* b, const double* c, double s, int64_t n, void* stream) {
+    clear_error();
+    if (n < 0) return fail(SB_ERR_ARGUMENT, "negative element count");
+    if (n == 0) return SB_OK;
+    if (!a || !b || !c) return fail(SB_ERR_ARGUMENT, "null pointer");
+    if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(c)) & 15)
+        return fail(SB_ERR_ARGUMENT, "triad arrays must be 16-byte aligned");
+    int* counters;
+    int sms;
+    int rc = get_counters(&counters, &sms);
+    if (rc) return rc;
+    triad_kernel<<<sms * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, b, c, s, n);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SB_OK : cuda_fail(e, "triad launch");
 }
 
 double* sb_host_alloc(int64_t count) {

@@ -16,6 +16,8 @@ bool tma_ok(const void* p, int64_t ni);
 int halo_copy(const double* src, double* dst, int ni, int nj, int nk, cudaStream_t st);
 int jacobi_run(double* a_buf, double* b_buf, int ni, int nj, int nk, int64_t iters, double a,
                double b, int depth, cudaStream_t st, int* in_b);
+int jacobi_generic_sweep(const double* src, double* dst, int ni, int nj, int nk, double a, double b,
+                         cudaStream_t st);
 int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,
            cudaStream_t st);
 

@@ -142,3 +142,27 @@ def test_device_errors_are_loud():
     lib = _lib.load()
     with pytest.raises(ValueError):
         _lib.check(lib.sb_run_host(0, 0, 4, 4, 4, 1, 0.0, 0.1, 1, 0))
+
+
+def test_line_level_api_matches_oracle():
+    """Line updates (reference kernels.py:212-247) vs the oracle's window
+    kernels, bitwise, on host and device grids."""
+    from paper_1004_1741_b200.grid import InitPattern, create_grid
+    from paper_1004_1741_b200.kernels import (gs_line_update, gs_line_update_interleaved,
+                                              jacobi_line_update)
+
+    g = create_grid(7, 6, 5, InitPattern.seeded_random(42, -1.0, 1.0))
+    for k, j in ((0, 0), (2, 3), (4, 5)):
+        # Jacobi line = one full oracle sweep restricted to that line
+        full = oracle.run_serial("jacobi", g.data, 1, 0.5, 0.1)
+        dst = create_grid(7, 6, 5, InitPattern.uniform(0))
+        jacobi_line_update(g, dst, StencilCoeffs(0.5, 0.1), k, j)
+        assert np.array_equal(dst.data[k + 1, j + 1, 1:-1], full[k + 1, j + 1, 1:-1])
+        for fn, kern in ((gs_line_update, "gs-naive"), (gs_line_update_interleaved, "gs-interleaved")):
+            h = g.copy()
+            fn(h, 1 / 6, k, j)
+            d = g.to_device()
+            fn(d, 1 / 6, k, j)
+            assert np.array_equal(h.data, d.data.cpu().numpy())
+            changed = np.argwhere(h.data != g.data)
+            assert set(map(tuple, changed[:, :2].tolist())) <= {(k + 1, j + 1)}
