@@ -43,6 +43,9 @@ def load():
     lib.sbo_run_threaded_jacobi.restype = i32
     lib.sbo_run_pipeline_gs.argtypes = [i32, vp, i64, i64, i64, i64, dbl, i32]
     lib.sbo_run_pipeline_gs.restype = i32
+    for name in ("sbo_gs_window", "sbo_gs_window_interleaved"):
+        getattr(lib, name).argtypes = [vp, vp, vp, i64, dbl, i64, i64]
+        getattr(lib, name).restype = None
     _lib = lib
     return lib
 
@@ -85,4 +88,16 @@ def run_threaded(kernel, data, iters, a=0.0, b=1.0 / 6.0, threads=None):
     rc = lib.sbo_run_pipeline_gs(KERNEL_IDS[kernel], g.ctypes.data, ni, nj, nk, iters, b, threads)
     if rc < 0:
         raise ValueError("partition error")
+    return g
+
+
+def gs_line(kernel, data, k, j, b):
+    """One in-place GS line update of interior line (k, j) (reference
+    kernels.py:236-247 via the window kernels).  Returns a new array."""
+    g = np.array(data, dtype=np.float64, order="C", copy=True)
+    ni, nj, nk = _check(g)
+    fn = load().sbo_gs_window_interleaved if kernel == "gs-interleaved" else load().sbo_gs_window
+    plane = (nj + 2) * (ni + 2) * 8
+    base = g.ctypes.data
+    fn(base + k * plane, base + (k + 1) * plane, base + (k + 2) * plane, ni + 2, b, j + 1, j + 2)
     return g
