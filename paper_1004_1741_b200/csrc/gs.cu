@@ -69,10 +69,12 @@ struct GsParams {
     unsigned long long* prof;  // SB_GS_PROFILE builds: per-CTA cycle counters
 };
 
-template <int BJ_, int BK_, int CW_, int NS_>
+template <int BJ_, int BK_, int CW_, int NS_, int LPT_>
 struct GsCfg {
-    static constexpr int BJ = BJ_, BK = BK_, CW = CW_, NS = NS_;
-    static constexpr int NCOMP = BJ * BK;                // compute threads (one per line)
+    static constexpr int BJ = BJ_, BK = BK_, CW = CW_, NS = NS_, LPT = LPT_;
+    static_assert(BK % LPT == 0, "lines per thread must divide the tile's planes");
+    static constexpr int NCOMP = BJ * BK / LPT;          // compute threads (LPT lines each:
+                                                         // planes kl, kl + BK/LPT, ...)
     static_assert(NCOMP % 32 == 0, "whole compute warps");
     static constexpr int NT = NCOMP + 64;                // + loader warp + storer warp
     static constexpr int LJ = BJ + 2, LK = BK + 2;       // lines incl. halo
@@ -247,6 +249,71 @@ __device__ void gs_storer(const CUtensorMap* st_map, const GsParams& p, double* 
     }
 }
 
+// One line of a tile as seen by its compute thread: column i at pi, column
+// i+1 (the E neighbour) at pe in chunk ce, the start of chunk ce+1 at pnext.
+struct GsLine {
+    double* pi;
+    double* pe;
+    double* pnext;
+    double wv;  // own previous value: the W neighbour
+    int i, ce, line;
+    bool in;    // inside the grid (partial tiles at the far edges)
+};
+
+template <class C>
+__device__ __forceinline__ void gs_line_init(GsLine& L, double* smem, uint32_t gc, int jl, int kl,
+                                             bool in) {
+    constexpr int NS = C::NS, CW = C::CW;
+    L.line = (kl + 1) * C::LJ + (jl + 1);
+    L.i = 1 - (jl + kl);
+    L.pi = smem + size_t(gc % NS) * C::SLOT + L.line * CW + max(L.i, 0);
+    L.pe = L.pi + 1;
+    L.ce = 0;
+    L.pnext = smem + size_t((gc + 1) % NS) * C::SLOT + L.line * CW;
+    L.wv = L.pi[-max(L.i, 0)];  // column 0: the Dirichlet halo (W of column 1)
+    L.in = in;
+}
+
+// update column L.i (if active) and advance the line by one column
+template <class C, bool INTERLEAVED, bool FULL>
+__device__ __forceinline__ void gs_line_step(GsLine& L, double* smem, uint32_t gc, double b, int ni) {
+    constexpr int NS = C::NS, CW = C::CW, LJ = C::LJ;
+    const bool active = FULL || (L.in && (L.i >= 1) && (L.i <= ni));
+    if (active) {
+        const double e = *L.pe;
+        const double sv = L.pi[-CW], nv = L.pi[CW];
+        const double dv = L.pi[-LJ * CW], uv = L.pi[LJ * CW];
+        double x;
+        if (INTERLEAVED) {  // (ni >= 2 on this path: ni+2 is even)
+            double tmp = __dadd_rn(e, sv);
+            tmp = __dadd_rn(tmp, nv);
+            tmp = __dadd_rn(tmp, dv);
+            tmp = __dadd_rn(tmp, uv);
+            x = __dmul_rn(b, __dadd_rn(L.wv, tmp));
+        } else {
+            double acc = __dadd_rn(L.wv, e);
+            acc = __dadd_rn(acc, sv);
+            acc = __dadd_rn(acc, nv);
+            acc = __dadd_rn(acc, dv);
+            acc = __dadd_rn(acc, uv);
+            x = __dmul_rn(b, acc);
+        }
+        *L.pi = x;
+        L.wv = x;
+    }
+    if (FULL || L.i >= 0) {  // advance: pi to column i+1, pe to column i+2
+        L.pi = L.pe;
+        if (((L.i + 2) & (CW - 1)) == 0) {
+            ++L.ce;
+            L.pe = L.pnext;
+            L.pnext = smem + size_t((gc + L.ce + 1) % NS) * C::SLOT + L.line * CW;
+        } else {
+            ++L.pe;
+        }
+    }
+    ++L.i;
+}
+
 // ---------------------------------------------------------------------------
 template <class C, bool INTERLEAVED>
 __global__ void __launch_bounds__(C::NT, 1)
@@ -281,14 +348,13 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
         return;
     }
 
-    // compute thread: one line of the tile.  All chunk waits and releases are
-    // CTA-uniform events (functions of the step only), handled by thread 0
+    // compute thread: LPT lines of the tile.  All chunk waits and releases
+    // are CTA-uniform events (functions of the step only), handled by thread 0
     // around the per-step named barrier: when the trailing line completes a
     // chunk, every thread fences its shared-memory writes for the async proxy
     // and after the barrier thread 0 hands the chunk to the storer.
-    const int jl = tid % BJ, kl = tid / BJ;
-    const int skew = jl + kl;
-    const int line = (kl + 1) * LJ + (jl + 1);
+    constexpr int LPT = C::LPT, KSTEP = C::BK / C::LPT;
+    const int jl = tid % BJ, kl0 = tid / BJ;
     const double b = p.b;
     const int nch = p.nch, ni = p.ni;
     const int nsteps = ni + SMAX;
@@ -312,17 +378,12 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
         q = (q + 1) % C::QS;
         if (t.s < 0) break;
         const int J0 = 1 + t.J * BJ, K0 = 1 + t.K * C::BK;
-        const bool line_in = (J0 + jl <= p.nj) && (K0 + kl <= p.nk);
-        // column i of this line at pi, column i+1 at pe (chunk ce).  The step
-        // loop runs in blocks of CW steps; the CTA-uniform events -- the leading
-        // line entering a new chunk, the trailing line completing one -- fall
-        // on fixed positions of a block.
-        int i = 1 - skew;
-        double* pi = smem + size_t(gc % NS) * C::SLOT + line * CW + max(i, 0);
-        double* pe = pi + 1;
-        int ce = 0;
-        double* pnext = smem + size_t((gc + 1) % NS) * C::SLOT + line * CW;  // start of chunk ce+1
-        double wv = pi[-max(i, 0)];  // column 0: the Dirichlet halo (W of column 1)
+        GsLine lines[LPT];
+#pragma unroll
+        for (int l = 0; l < LPT; ++l) {
+            const int kl = kl0 + l * KSTEP;
+            gs_line_init<C>(lines[l], smem, gc, jl, kl, (J0 + jl <= p.nj) && (K0 + kl <= p.nk));
+        }
         int ready = 1;               // chunks known loaded (thread 0)
         int completed = 0;           // chunks completed so far
         int released = 0;            // chunks handed to the storer (thread 0)
@@ -333,45 +394,14 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
         auto block = [&](const int st0, auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-            for (int pos = 0; pos < CW; ++pos, ++i) {
+            for (int pos = 0; pos < CW; ++pos) {
                 const int st = st0 + pos;
                 if (pos == POS_FIN + 1 || pos == 0) {  // every thread fenced before the last barrier
                     if (tid == 0)
                         while (released < completed) mbar_arrive(&done[(gc + released++) % NS]);
                 }
-                const bool active = FULL || (line_in && (i >= 1) && (i <= ni));
-                if (active) {
-                    const double e = *pe;
-                    const double sv = pi[-CW], nv = pi[CW];
-                    const double dv = pi[-LJ * CW], uv = pi[LJ * CW];
-                    double x;
-                    if (INTERLEAVED) {  // (ni >= 2 on this path: ni+2 is even)
-                        double tmp = __dadd_rn(e, sv);
-                        tmp = __dadd_rn(tmp, nv);
-                        tmp = __dadd_rn(tmp, dv);
-                        tmp = __dadd_rn(tmp, uv);
-                        x = __dmul_rn(b, __dadd_rn(wv, tmp));
-                    } else {
-                        double acc = __dadd_rn(wv, e);
-                        acc = __dadd_rn(acc, sv);
-                        acc = __dadd_rn(acc, nv);
-                        acc = __dadd_rn(acc, dv);
-                        acc = __dadd_rn(acc, uv);
-                        x = __dmul_rn(b, acc);
-                    }
-                    *pi = x;
-                    wv = x;
-                }
-                if (FULL || i >= 0) {  // advance: pi to column i+1, pe to column i+2
-                    pi = pe;
-                    if (((i + 2) & (CW - 1)) == 0) {
-                        ++ce;
-                        pe = pnext;
-                        pnext = smem + size_t((gc + ce + 1) % NS) * C::SLOT + line * CW;
-                    } else {
-                        ++pe;
-                    }
-                }
+#pragma unroll
+                for (int l = 0; l < LPT; ++l) gs_line_step<C, INTERLEAVED, FULL>(lines[l], smem, gc, b, ni);
                 if (pos == POS_FIN || (!FULL && st == nsteps - 1)) {
                     const int fin = (st >= nsteps - 1) ? nch : min(nch, max(0, (st + 2 - SMAX) / CW));
                     if (fin > completed) {
@@ -453,7 +483,7 @@ __global__ void gs_serial_kernel(double* g, int ni, int nj, int nk, int sweeps, 
 }
 
 // ---------------------------------------------------------------------------
-using GsC = GsCfg<16, 16, 16, 5>;  // CW = 16: 128-B lines (TMA smem addresses must be 128-B aligned)
+using GsC = GsCfg<16, 16, 16, 5, 1>;  // CW = 16: 128-B lines (TMA smem addresses must be 128-B aligned)
 
 struct GsScratch {
     int* words = nullptr;  // ticket, err
