@@ -41,6 +41,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include <utility>
 #include <cstdint>
@@ -502,24 +503,35 @@ extern "C" void sb_gs_profile(unsigned long long* out) {
 }
 #endif
 
-// Ticket order over `sweeps` sweeps of a tiles_j x tiles_k tile grid: by
-// tau = (J + K) + 2 * sweep, then sweep, then J.  Every dependency of task
+// Ticket order over `sweeps` sweeps of a tiles_j x tiles_k tile grid, in
+// windows of `window` sweeps: inside a window by tau = (J + K) + 2 * sweep,
+// then sweep, then J; windows one after another.  Every dependency of task
 // (s, J, K) -- (s, J-1, K), (s, J, K-1) at tau-1, (s-1, J+1, K), (s-1, J, K+1)
-// at tau-1, (s-1, J, K) at tau-2, (s-R+1, J, K) at tau-2(R-1) -- has a smaller
-// ticket, so a persistent grid cannot deadlock, and successive sweeps advance
-// together in a diagonal band instead of one whole wavefront after another.
-static std::vector<int2> wavefront_order(int tiles_j, int tiles_k, int sweeps) {
+// at tau-1, (s-1, J, K) at tau-2, (s-R+1, J, K) at tau-2(R-1), or an earlier
+// window -- has a smaller ticket, so a persistent grid cannot deadlock.
+// Successive sweeps advance together in a diagonal band (the paper's
+// multi-wavefront GS); the window bounds how many are in flight, so that a
+// tile's next sweep reads its previous sweep's data while it is still in L2.
+static std::vector<int2> wavefront_order(int tiles_j, int tiles_k, int sweeps, int window) {
     std::vector<int2> ord;
     ord.reserve(size_t(sweeps) * tiles_j * tiles_k);
     const int dmax = tiles_j + tiles_k - 2;
-    for (int tau = 0; tau <= dmax + 2 * (sweeps - 1); ++tau)
-        for (int s = std::max(0, (tau - dmax + 1) / 2); s < sweeps && 2 * s <= tau; ++s) {
-            const int d = tau - 2 * s;
-            if (d > dmax) continue;
-            for (int J = std::max(0, d - (tiles_k - 1)); J < tiles_j && J <= d; ++J)
-                ord.push_back(make_int2(s, J | ((d - J) << 16)));
-        }
+    for (int s0 = 0; s0 < sweeps; s0 += window) {
+        const int ns = std::min(window, sweeps - s0);
+        for (int tau = 0; tau <= dmax + 2 * (ns - 1); ++tau)
+            for (int s = std::max(0, (tau - dmax + 1) / 2); s < ns && 2 * s <= tau; ++s) {
+                const int d = tau - 2 * s;
+                if (d > dmax) continue;
+                for (int J = std::max(0, d - (tiles_k - 1)); J < tiles_j && J <= d; ++J)
+                    ord.push_back(make_int2(s0 + s, J | ((d - J) << 16)));
+            }
+    }
     return ord;
+}
+
+static int gs_window() {
+    static int w = getenv("SB_GS_WINDOW") ? std::max(1, atoi(getenv("SB_GS_WINDOW"))) : 4;
+    return w;
 }
 
 template <class C>
@@ -552,7 +564,7 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
         std::min<int64_t>(512, ((int64_t(1) << 30) / (nch64 + 1)) - 2), (int64_t(1) << 26) / ntiles));
     const int batch = (int)std::min<int64_t>(iters, per_launch);
     if (S.tj != tiles_j || S.tk != tiles_k || S.ns != batch) {
-        const std::vector<int2> ord = wavefront_order(tiles_j, tiles_k, batch);
+        const std::vector<int2> ord = wavefront_order(tiles_j, tiles_k, batch, gs_window());
         if (S.order_cap < ord.size()) {
             if (S.order) cudaFree(S.order);
             if ((e = cudaMalloc(&S.order, ord.size() * sizeof(int2))) != cudaSuccess)
@@ -610,7 +622,7 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
     for (int64_t done = 0; done < iters;) {
         const int n = (int)std::min<int64_t>(iters - done, batch);
         if (n != S.ns) {  // a shorter final batch needs its own order table
-            const std::vector<int2> ord = wavefront_order(tiles_j, tiles_k, n);
+            const std::vector<int2> ord = wavefront_order(tiles_j, tiles_k, n, gs_window());
             if ((e = cudaMemcpyAsync(S.order, ord.data(), ord.size() * sizeof(int2), cudaMemcpyHostToDevice,
                                      st)) != cudaSuccess)
                 return cuda_fail(e, "cudaMemcpy(order)");
