@@ -17,8 +17,10 @@
 //   * a thread owns RJ consecutive rows, so N/S neighbours are registers,
 //     except at warp-strip boundaries, which go through a small
 //     double-buffered shared "exchange" row per warp and level;
-//   * the z-queue (planes k-1, k, k+1 of the level below) lives in
-//     registers; levels trail by one plane, one __syncthreads per plane;
+//   * the z-queues (planes k-1, k, k+1 of the level below) live in
+//     registers -- for level 1 optionally not: it can read the TMA ring
+//     directly (JacobiCfg::L1S); levels trail by one plane, one
+//     __syncthreads per plane;
 //   * output rows leave with coalesced 16-byte global stores.
 // Overlapped (trapezoid) tiling: level L is valid on the tile grown by T-L
 // cells; rows outside that region skip their arithmetic.
@@ -35,7 +37,7 @@
 // Work distribution: persistent CTAs grab (tile, k-block) items from a
 // global atomic counter in k-block-major order (CTAs running together hold
 // neighbouring tiles of the same planes, so overlapping halo reads hit L2).
-// The TMA producer runs S-1 planes ahead, across item boundaries.
+// The TMA producer runs C::AHEAD planes ahead, across item boundaries.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -57,9 +59,15 @@ struct JacobiParams {
     double* dst;             // output grid
 };
 
-template <int T_, int RJ_, int NW_, int S_, int MINB_>
+template <int T_, int RJ_, int NW_, int S_, int MINB_, bool L1S_ = false>
 struct JacobiCfg {
     static constexpr int T = T_, RJ = RJ_, NW = NW_, S = S_, MINB = MINB_;
+    // L1S: level 1 reads planes k-1, k, k+1 from the ring (three live slots,
+    // prefetch distance S-2) instead of a register queue (prefetch S-1):
+    // fewer registers (more warps / CTAs per SM), more shared-memory loads
+    static constexpr bool L1S = L1S_;
+    static constexpr int NQ = L1S ? (T > 1 ? T - 1 : 1) : T;  // register queues
+    static constexpr int AHEAD = L1S ? S - 2 : S - 1;         // TMA prefetch distance
     static constexpr int H = (T + 1) / 2 * 2;          // input halo along i (even: TMA boxes
                                                        // must start 16-byte aligned)
     static constexpr int BW = 64;                      // cells per warp row (32 lanes x 2)
@@ -67,6 +75,7 @@ struct JacobiCfg {
     static constexpr int ROWS = NW * RJ;               // rows computed per tile (level-1 region)
     static constexpr int TJ = ROWS - 2 * (T - 1);      // output rows per tile
     static_assert(TJ >= 1, "tile too short for this depth");
+    static_assert(S_ >= (L1S_ ? 3 : 2), "ring too small");
     static constexpr int BH = ROWS + 2;                // input box rows (+1 neighbour row each side)
     static constexpr int BOX = BW * BH;
     static constexpr int BOXS = (BOX + 15) / 16 * 16;  // 128-B aligned TMA destinations
@@ -163,14 +172,63 @@ __device__ __forceinline__ void produce(const CUtensorMap* src_map, const Jacobi
     }
 }
 
+// One level's update of a thread's RJ rows x 2 cells.  cen: the centre
+// plane with the south (row 0) and north (row RJ+1) neighbour rows; dn/up:
+// the planes below and above.
+template <class C, bool FAST, bool AZ>
+__device__ __forceinline__ void level_update(const double (&cen)[C::RJ + 2][2],
+                                             const double (&dn)[C::RJ][2],
+                                             const double (&up)[C::RJ][2], double (&nv)[C::RJ][2],
+                                             double a, double b, int L, int dj, int k, int gj,
+                                             bool in_i0, bool in_i1, const JacobiParams& p) {
+    constexpr int T = C::T, RJ = C::RJ;
+#pragma unroll
+    for (int r = 0; r < RJ; ++r) {
+        const double c0 = cen[r + 1][0], c1 = cen[r + 1][1];
+        const double wv = __shfl_up_sync(0xffffffffu, c1, 1);    // cell i-1 (lane-1)
+        const double ev = __shfl_down_sync(0xffffffffu, c0, 1);  // cell i+2 (lane+1)
+        bool compute = true;
+        if (!FAST) {
+            const int jr = dj + r, need = T - L;
+            compute = (jr >= -need) && (jr < C::TJ + need) && (k >= 1) && (k <= p.nk) &&
+                      (gj + r >= 1) && (gj + r <= p.nj);
+        }
+        if (compute) {
+            double acc0 = __dadd_rn(wv, c1), acc1 = __dadd_rn(c0, ev);
+            acc0 = __dadd_rn(acc0, cen[r][0]);
+            acc1 = __dadd_rn(acc1, cen[r][1]);
+            acc0 = __dadd_rn(acc0, cen[r + 2][0]);
+            acc1 = __dadd_rn(acc1, cen[r + 2][1]);
+            acc0 = __dadd_rn(acc0, dn[r][0]);
+            acc1 = __dadd_rn(acc1, dn[r][1]);
+            acc0 = __dadd_rn(acc0, up[r][0]);
+            acc1 = __dadd_rn(acc1, up[r][1]);
+            const double o0 = jac_final<AZ>(a, b, c0, acc0);
+            const double o1 = jac_final<AZ>(a, b, c1, acc1);
+            if (FAST) {
+                nv[r][0] = o0;
+                nv[r][1] = o1;
+            } else {
+                nv[r][0] = in_i0 ? o0 : c0;
+                nv[r][1] = in_i1 ? o1 : c1;
+            }
+        } else {
+            nv[r][0] = c0;  // halo rows/planes keep their value; unneeded rows: anything
+            nv[r][1] = c1;
+        }
+    }
+}
+
 // One plane step of the current item.  FAST: every cell the tile computes
 // this item is interior (no Dirichlet masks, no trapezoid row skipping).
-// PH = g mod 3 selects the register rotation statically.  Returns true when
-// the item is finished.
+// PH = g mod 3 selects the register rotation statically.  With C::L1S level
+// 1 reads its three input planes straight from the TMA ring (slots g-2,
+// g-1, g); otherwise from register queue Q[0], fed from ring slot g.
 template <class C, bool FAST, bool AZ, int PH>
 __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const JacobiParams& p,
                                             double* ring, double* xb, uint64_t* full,
-                                            ItemInfo* queue, LevelQ<C> (&Q)[C::T], JState& s) {
+                                            ItemInfo* queue, LevelQ<C> (&Q)[C::NQ],
+                                            JState& s) {
     constexpr int T = C::T, RJ = C::RJ, NW = C::NW, S = C::S, BW = C::BW;
     constexpr int D = PH % 3, CC = (PH + 1) % 3, U = (PH + 2) % 3;
     const int tid = threadIdx.x;
@@ -181,77 +239,70 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
     const int dj = -(T - 1) + w * RJ;
     const ItemInfo& it = s.it;
 
-    const int slot = s.g % S, pslot = (s.g + S - 1) % S;
+    const int slot = s.g % S;
     mbar_wait(&full[slot], (s.g / S) & 1);
     const double* cur = ring + size_t(slot) * C::BOXS;
-    const double* prv = ring + size_t(pslot) * C::BOXS;
+    const double* prv = ring + size_t((s.g + S - 1) % S) * C::BOXS;
+    const double* pp = ring + size_t((s.g + S - 2) % S) * C::BOXS;
     const int pplane = it.kb - T + s.n;
     const int gi = it.I0 + di, gj = it.J0 + dj;
     const bool in_i0 = (gi >= 1) && (gi <= p.ni);
     const bool in_i1 = (gi + 1 >= 1) && (gi + 1 <= p.ni);
     const double a = p.a, b = p.b;
-
+    if (!C::L1S) {
 #pragma unroll
-    for (int r = 0; r < RJ; ++r) {
-        const double2 x = lds2(cur + (brow + r) * BW + col);
-        Q[0].q[U][r][0] = x.x;
-        Q[0].q[U][r][1] = x.y;
+        for (int r = 0; r < RJ; ++r) {
+            const double2 x = lds2(cur + (brow + r) * BW + col);
+            Q[0].q[U][r][0] = x.x;
+            Q[0].q[U][r][1] = x.y;
+        }
     }
 
 #pragma unroll
     for (int L = 1; L <= T; ++L) {
-        LevelQ<C>& In = Q[L - 1];
         const int k = pplane - L;
-        double sT0, sT1, nB0, nB1;
-        if (L == 1) {
-            const double2 s2 = lds2(prv + (brow - 1) * BW + col);
-            const double2 n2 = lds2(prv + (brow + RJ) * BW + col);
-            sT0 = s2.x; sT1 = s2.y; nB0 = n2.x; nB1 = n2.y;
-        } else {
-            const double* xr = xb + (size_t((L - 2) * 2 + ((s.g + 1) & 1)) * NW) * C::XROW;
-            const double2 s2 = lds2(xr + max(w - 1, 0) * C::XROW + BW + col);
-            const double2 n2 = lds2(xr + min(w + 1, NW - 1) * C::XROW + col);
-            sT0 = s2.x; sT1 = s2.y; nB0 = n2.x; nB1 = n2.y;
-        }
         double nv[RJ][2];
+        if (C::L1S && L == 1) {
+            double cen[RJ + 2][2], dn[RJ][2], up[RJ][2];
 #pragma unroll
-        for (int r = 0; r < RJ; ++r) {
-            const double c0 = In.q[CC][r][0], c1 = In.q[CC][r][1];
-            const double wv = __shfl_up_sync(0xffffffffu, c1, 1);    // cell i-1 (lane-1)
-            const double ev = __shfl_down_sync(0xffffffffu, c0, 1);  // cell i+2 (lane+1)
-            const double s0 = (r > 0) ? In.q[CC][r - 1][0] : sT0;
-            const double s1 = (r > 0) ? In.q[CC][r - 1][1] : sT1;
-            const double n0 = (r + 1 < RJ) ? In.q[CC][r + 1][0] : nB0;
-            const double n1 = (r + 1 < RJ) ? In.q[CC][r + 1][1] : nB1;
-            bool compute = true;
-            if (!FAST) {
-                const int jr = dj + r, need = T - L;
-                compute = (jr >= -need) && (jr < C::TJ + need) && (k >= 1) && (k <= p.nk) &&
-                          (gj + r >= 1) && (gj + r <= p.nj);
+            for (int r = 0; r < RJ + 2; ++r) {
+                const double2 x = lds2(prv + (brow - 1 + r) * BW + col);
+                cen[r][0] = x.x;
+                cen[r][1] = x.y;
             }
-            if (compute) {
-                double acc0 = __dadd_rn(wv, c1), acc1 = __dadd_rn(c0, ev);
-                acc0 = __dadd_rn(acc0, s0);
-                acc1 = __dadd_rn(acc1, s1);
-                acc0 = __dadd_rn(acc0, n0);
-                acc1 = __dadd_rn(acc1, n1);
-                acc0 = __dadd_rn(acc0, In.q[D][r][0]);
-                acc1 = __dadd_rn(acc1, In.q[D][r][1]);
-                acc0 = __dadd_rn(acc0, In.q[U][r][0]);
-                acc1 = __dadd_rn(acc1, In.q[U][r][1]);
-                const double o0 = jac_final<AZ>(a, b, c0, acc0);
-                const double o1 = jac_final<AZ>(a, b, c1, acc1);
-                if (FAST) {
-                    nv[r][0] = o0;
-                    nv[r][1] = o1;
-                } else {
-                    nv[r][0] = in_i0 ? o0 : c0;
-                    nv[r][1] = in_i1 ? o1 : c1;
-                }
+#pragma unroll
+            for (int r = 0; r < RJ; ++r) {
+                const double2 x = lds2(pp + (brow + r) * BW + col);
+                const double2 y = lds2(cur + (brow + r) * BW + col);
+                dn[r][0] = x.x;
+                dn[r][1] = x.y;
+                up[r][0] = y.x;
+                up[r][1] = y.y;
+            }
+            level_update<C, FAST, AZ>(cen, dn, up, nv, a, b, L, dj, k, gj, in_i0, in_i1, p);
+        } else {
+            LevelQ<C>& In = Q[C::L1S ? L - 2 : L - 1];
+            double2 s2, n2;
+            if (L == 1) {  // neighbour rows of the input plane: from the ring
+                s2 = lds2(prv + (brow - 1) * BW + col);
+                n2 = lds2(prv + (brow + RJ) * BW + col);
             } else {
-                nv[r][0] = c0;  // halo rows/planes keep their value; unneeded rows: anything
-                nv[r][1] = c1;
+                const double* xr = xb + (size_t((L - 2) * 2 + ((s.g + 1) & 1)) * NW) * C::XROW;
+                s2 = lds2(xr + max(w - 1, 0) * C::XROW + BW + col);
+                n2 = lds2(xr + min(w + 1, NW - 1) * C::XROW + col);
             }
+            double cen[RJ + 2][2];
+            cen[0][0] = s2.x;
+            cen[0][1] = s2.y;
+            cen[RJ + 1][0] = n2.x;
+            cen[RJ + 1][1] = n2.y;
+#pragma unroll
+            for (int r = 0; r < RJ; ++r) {
+                cen[r + 1][0] = In.q[CC][r][0];
+                cen[r + 1][1] = In.q[CC][r][1];
+            }
+            level_update<C, FAST, AZ>(cen, In.q[D], In.q[U], nv, a, b, L, dj, k, gj, in_i0, in_i1,
+                                      p);
         }
         if (L < T) {
             double* xw = xb + (size_t((L - 1) * 2 + (s.g & 1)) * NW + w) * C::XROW;
@@ -259,8 +310,8 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
             sts2(xw + BW + col, nv[RJ - 1][0], nv[RJ - 1][1]);
 #pragma unroll
             for (int r = 0; r < RJ; ++r) {
-                Q[L].q[U][r][0] = nv[r][0];
-                Q[L].q[U][r][1] = nv[r][1];
+                Q[C::L1S ? L - 1 : L].q[U][r][0] = nv[r][0];
+                Q[C::L1S ? L - 1 : L].q[U][r][1] = nv[r][1];
             }
         } else if (s.n >= 2 * T) {
             if (di >= 0 && di < C::TO && gi + 1 <= p.ni + 1) {
@@ -277,6 +328,7 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
         }
     }
     __syncthreads();
+    // the oldest ring slot (g-2 with L1S, else g-1) is free now: refill it
     if (tid == 0 && s.pitem.N > 0) produce<C>(src_map, p, ring, full, queue, s);
     ++s.g;
     return ++s.n == it.N;
@@ -287,8 +339,8 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
 template <class C, bool FAST, bool AZ>
 __device__ __forceinline__ void jacobi_steps(const CUtensorMap* src_map, const JacobiParams& p,
                                              double* ring, double* xb, uint64_t* full,
-                                             ItemInfo* queue, LevelQ<C> (&Q)[C::T], JState& s,
-                                             int count) {
+                                             ItemInfo* queue, LevelQ<C> (&Q)[C::NQ],
+                                             JState& s, int count) {
     if (count <= 0) return;
     const int ph = s.g % 3;
     if (ph == 1) {
@@ -331,13 +383,13 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map, const JacobiParams
         fence_mbar_init();
         s.pitem = decode_item<C>(p, atomicAdd(p.counter, 1));
         queue[0] = s.pitem;
-        while (s.ld_issued < S - 1 && s.pitem.N > 0) produce<C>(&src_map, p, ring, full, queue, s);
+        while (s.ld_issued < C::AHEAD && s.pitem.N > 0) produce<C>(&src_map, p, ring, full, queue, s);
     }
     __syncthreads();
 
-    LevelQ<C> Q[T];
+    LevelQ<C> Q[C::NQ];
 #pragma unroll
-    for (int L = 0; L < T; ++L)
+    for (int L = 0; L < C::NQ; ++L)
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll

@@ -282,13 +282,18 @@ static int launch_depth(int T, const double* src, double* dst, int ni, int nj, i
             if (v == 1) SB_L(1, 2, 8, 4, 4);
             SB_L(1, 4, 8, 4, 2);
         case 2:
-            if (v == 1) SB_L(2, 2, 16, 4, 1);
-            SB_L(2, 4, 8, 4, 2);
+            if (v == 1) SB_L(2, 4, 8, 4, 2);
+            if (v == 2) SB_L(2, 4, 12, 5, 1, true);
+            SB_L(2, 4, 8, 4, 2, true);
         case 3:
-            if (v == 1) SB_L(3, 4, 8, 4, 1);
-            SB_L(3, 2, 16, 4, 1);
+            if (v == 1) SB_L(3, 2, 16, 4, 1);
+            if (v == 2) SB_L(3, 3, 16, 5, 1, true);
+            if (v == 3) SB_L(3, 4, 8, 4, 2, true);
+            SB_L(3, 4, 12, 5, 1, true);
         case 4:
             if (v == 1) SB_L(4, 2, 16, 4, 1);
+            if (v == 2) SB_L(4, 4, 12, 5, 1, true);
+            if (v == 3) SB_L(4, 3, 16, 5, 1, true);
             SB_L(4, 4, 8, 4, 1);
         case 5: SB_L(5, 2, 12, 3, 1);
         case 6: SB_L(6, 2, 12, 3, 1);
