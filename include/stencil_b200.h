@@ -86,8 +86,10 @@ int sb_max_depth(void);
  * Jacobi sweeps on device memory.  `grid` and `scratch` are device
  * pointers to two distinct padded grids; `scratch` needs no initialisation
  * (its halo is copied from `grid` on the stream).  Advances `iters` sweeps,
- * fusing up to `depth` (1..sb_max_depth()) sweeps per HBM pass; iters that
- * are not a multiple of depth end with shallower passes.  On return
+ * fusing up to `depth` (1..sb_max_depth()) sweeps per HBM pass (depths
+ * above 4 run as 4-sweep passes, the fastest fused depth on B200; results
+ * are identical for every depth); iters that are not a multiple of the
+ * pass depth end with a shallower pass.  On return
  * *result_in_scratch tells which buffer holds the final field (the other
  * holds an intermediate one), like run_serial returning the copy for odd
  * iteration counts.  Asynchronous on `stream`.

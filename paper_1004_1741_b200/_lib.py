@@ -19,7 +19,8 @@ from .errors import (
     PlanError,
 )
 
-LIB_PATH = Path(__file__).resolve().parent / "libsb200.so"
+# SB200_LIB: load an alternative build (experiments); default: the in-tree library
+LIB_PATH = Path(os.environ.get("SB200_LIB") or Path(__file__).resolve().parent / "libsb200.so")
 
 SB_OK = 0
 KERNEL_IDS = {"jacobi": 0, "gs-naive": 1, "gs-interleaved": 2}

@@ -57,6 +57,7 @@ struct JacobiParams {
     double a, b;
     int* counter;            // work counter (zeroed before launch)
     double* dst;             // output grid
+    int64_t plane;           // (nj + 2) * (ni + 2) cells, < 2^31 (check_dims)
 };
 
 template <int T_, int RJ_, int NW_, int S_, int MINB_, bool L1S_ = false>
@@ -67,7 +68,9 @@ struct JacobiCfg {
     // fewer registers (more warps / CTAs per SM), more shared-memory loads
     static constexpr bool L1S = L1S_;
     static constexpr int NQ = L1S ? (T > 1 ? T - 1 : 1) : T;  // register queues
-    static constexpr int AHEAD = L1S ? S - 2 : S - 1;         // TMA prefetch distance
+    // TMA prefetch distance: the ring slots still being read limit it
+    static constexpr int AHEAD = L1S ? S - 2 : S - 1;
+    static_assert(AHEAD >= 1, "ring too small");
     static constexpr int H = (T + 1) / 2 * 2;          // input halo along i (even: TMA boxes
                                                        // must start 16-byte aligned)
     static constexpr int BW = 64;                      // cells per warp row (32 lanes x 2)
@@ -82,11 +85,14 @@ struct JacobiCfg {
     static constexpr int NT = NW * 32;
     static constexpr int XROW = 2 * BW;                // exchange doubles per warp: top + bottom row
     static constexpr int NX = (T > 1) ? (T - 1) : 0;   // levels with exchange rows (1..T-1)
+    static constexpr int XSLOT = NW;                   // one slot per warp
+    static constexpr int XB = 2;                       // exchange buffers (step parity)
     static constexpr int QSLOTS = 4;
     static constexpr size_t RING_OFF = 0;
     static constexpr size_t X_OFF = RING_OFF + size_t(S) * BOXS;
-    static constexpr size_t DBL_END = X_OFF + size_t(NX) * 2 * NW * XROW;
-    static constexpr size_t SMEM_BYTES = DBL_END * 8 + 8 * S + 16 * QSLOTS + 64;
+    static constexpr size_t DBL_END = X_OFF + size_t(NX) * XB * XSLOT * XROW;
+    // doubles, then queue[QSLOTS], mbarriers full[S], then the producer state
+    static constexpr size_t SMEM_BYTES = DBL_END * 8 + 16 * QSLOTS + 8 * S + 32 + 64;
     static constexpr uint32_t BOX_BYTES = uint32_t(BOX) * 8;
 };
 
@@ -146,29 +152,67 @@ __device__ __forceinline__ double jac_final(double a, double b, double c, double
     return __dadd_rn(__dmul_rn(a, c), __dmul_rn(b, acc));
 }
 
-struct JState {      // per-CTA loop state shared by the step functions
+struct JState {      // per-thread loop state shared by the step functions
     uint32_t g;      // global plane-step counter (ring phase, exchange parity, rotation)
     int n, cq;       // step within the item, consumer queue slot
     ItemInfo it;     // current item
-    uint32_t ld_issued;
-    int pq, pn;      // producer queue slot / plane step
-    ItemInfo pitem;  // producer's item
+    uint32_t ooff;   // this thread's output cell (row 0) within a plane
+    uint32_t omask;  // bit r: row r of this thread is an output row of the current item
 };
+
+// The TMA producer's state.  Only thread 0 produces, so it lives in shared
+// memory instead of occupying registers in every thread.
+struct Prod {
+    uint32_t ld_issued;  // plane loads issued
+    int pq, pn;          // queue slot / plane step of the producer's item
+    ItemInfo pitem;      // producer's item
+};
+
+// Per-item output addressing of a thread (hoisted out of the plane steps).
+template <class C>
+__device__ __forceinline__ void item_output(const JacobiParams& p, JState& s) {
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, w = tid >> 5;
+    const int di = 2 * lane - C::H;
+    const int dj = -(C::T - 1) + w * C::RJ;
+    const int gi = s.it.I0 + di, gj = s.it.J0 + dj;
+    uint32_t m = 0;
+    if (di >= 0 && di < C::TO && gi + 1 <= p.ni + 1) {
+#pragma unroll
+        for (int r = 0; r < C::RJ; ++r)
+            if (dj + r >= 0 && dj + r < C::TJ && gj + r <= p.nj) m |= 1u << r;
+    }
+    s.omask = m;
+    s.ooff = uint32_t(gj * (p.ni + 2) + gi);
+}
+
+// The producer's next work item.
+template <class C>
+__device__ __forceinline__ void next_item(const JacobiParams& p, ItemInfo* queue, Prod& pr) {
+    pr.pitem = decode_item<C>(p, atomicAdd(p.counter, 1));
+    queue[pr.pq] = pr.pitem;
+}
+
+template <class C>
+__device__ __forceinline__ Prod* prod_state(uint64_t* full) {
+    return reinterpret_cast<Prod*>(full + C::S);
+}
 
 template <class C>
 __device__ __forceinline__ void produce(const CUtensorMap* src_map, const JacobiParams& p,
-                                        double* ring, uint64_t* full, ItemInfo* queue, JState& s) {
+                                        double* ring, uint64_t* full, ItemInfo* queue) {
     constexpr int S = C::S;
-    uint64_t* bar = &full[s.ld_issued % S];
+    Prod& pr = *prod_state<C>(full);
+    if (pr.pitem.N <= 0) return;
+    uint64_t* bar = &full[pr.ld_issued % S];
     mbar_arrive_expect_tx(bar, C::BOX_BYTES);
-    tma_load_3d(ring + size_t(s.ld_issued % S) * C::BOXS, src_map, s.pitem.I0 - C::H,
-                s.pitem.J0 - C::T, s.pitem.kb - C::T + s.pn, bar);
-    ++s.ld_issued;
-    if (++s.pn == s.pitem.N) {
-        s.pn = 0;
-        s.pq = (s.pq + 1) % C::QSLOTS;
-        s.pitem = decode_item<C>(p, atomicAdd(p.counter, 1));
-        queue[s.pq] = s.pitem;
+    tma_load_3d(ring + size_t(pr.ld_issued % S) * C::BOXS, src_map, pr.pitem.I0 - C::H,
+                pr.pitem.J0 - C::T, pr.pitem.kb - C::T + pr.pn, bar);
+    ++pr.ld_issued;
+    if (++pr.pn == pr.pitem.N) {
+        pr.pn = 0;
+        pr.pq = (pr.pq + 1) % C::QSLOTS;
+        next_item<C>(p, queue, pr);
     }
 }
 
@@ -238,6 +282,8 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
     const int di = col - C::H;
     const int dj = -(T - 1) + w * RJ;
     const ItemInfo& it = s.it;
+    // exchange buffers: written this step / written by the previous step
+    const int xwb = int(s.g & 1), xrb = int((s.g + 1) & 1);
 
     const int slot = s.g % S;
     mbar_wait(&full[slot], (s.g / S) & 1);
@@ -287,7 +333,10 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
                 s2 = lds2(prv + (brow - 1) * BW + col);
                 n2 = lds2(prv + (brow + RJ) * BW + col);
             } else {
-                const double* xr = xb + (size_t((L - 2) * 2 + ((s.g + 1) & 1)) * NW) * C::XROW;
+                // south neighbour row: bottom row of warp w-1, north: top row of
+                // warp w+1 (clamped at the tile edge: those rows lie outside the
+                // trapezoid and their values are never used)
+                const double* xr = xb + size_t((L - 2) * C::XB + xrb) * C::XSLOT * C::XROW;
                 s2 = lds2(xr + max(w - 1, 0) * C::XROW + BW + col);
                 n2 = lds2(xr + min(w + 1, NW - 1) * C::XROW + col);
             }
@@ -305,7 +354,8 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
                                       p);
         }
         if (L < T) {
-            double* xw = xb + (size_t((L - 1) * 2 + (s.g & 1)) * NW + w) * C::XROW;
+            double* xl = xb + size_t((L - 1) * C::XB + xwb) * C::XSLOT * C::XROW;
+            double* xw = xl + w * C::XROW;
             sts2(xw + col, nv[0][0], nv[0][1]);
             sts2(xw + BW + col, nv[RJ - 1][0], nv[RJ - 1][1]);
 #pragma unroll
@@ -313,23 +363,20 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
                 Q[C::L1S ? L - 1 : L].q[U][r][0] = nv[r][0];
                 Q[C::L1S ? L - 1 : L].q[U][r][1] = nv[r][1];
             }
-        } else if (s.n >= 2 * T) {
-            if (di >= 0 && di < C::TO && gi + 1 <= p.ni + 1) {
-                const int64_t nip = p.ni + 2;
-                double* o = p.dst + ((int64_t)k * (p.nj + 2)) * nip + gi;
+        } else if (s.n >= 2 * T && s.omask) {
+            double* plane = p.dst + (int64_t)k * p.plane;  // CTA-uniform
+            uint32_t o = s.ooff;
 #pragma unroll
-                for (int r = 0; r < RJ; ++r) {
-                    const int jr = dj + r;
-                    if (jr >= 0 && jr < C::TJ && gj + r <= p.nj)
-                        *reinterpret_cast<double2*>(o + (int64_t)(gj + r) * nip) =
-                            make_double2(nv[r][0], nv[r][1]);
-                }
+            for (int r = 0; r < RJ; ++r) {
+                if (s.omask & (1u << r))
+                    *reinterpret_cast<double2*>(plane + o) = make_double2(nv[r][0], nv[r][1]);
+                o += uint32_t(p.ni + 2);
             }
         }
     }
     __syncthreads();
     // the oldest ring slot (g-2 with L1S, else g-1) is free now: refill it
-    if (tid == 0 && s.pitem.N > 0) produce<C>(src_map, p, ring, full, queue, s);
+    if (tid == 0) produce<C>(src_map, p, ring, full, queue);
     ++s.g;
     return ++s.n == it.N;
 }
@@ -369,21 +416,23 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map, const JacobiParams
     extern __shared__ __align__(128) double smem[];
     double* ring = smem + C::RING_OFF;
     double* xb = smem + C::X_OFF;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DBL_END);
-    ItemInfo* queue = reinterpret_cast<ItemInfo*>(full + S);
+    // queue[QSLOTS] (16-byte entries, 128-byte aligned), full[S], qbar[QSLOTS]
+    ItemInfo* queue = reinterpret_cast<ItemInfo*>(smem + C::DBL_END);
+    uint64_t* full = reinterpret_cast<uint64_t*>(queue + C::QSLOTS);
     const int tid = threadIdx.x;
 
     JState s;
-    s.ld_issued = 0;
-    s.pq = s.pn = 0;
-    s.pitem.N = 0;
     if (tid == 0) {
         tma_prefetch_desc(&src_map);
         for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
         fence_mbar_init();
-        s.pitem = decode_item<C>(p, atomicAdd(p.counter, 1));
-        queue[0] = s.pitem;
-        while (s.ld_issued < C::AHEAD && s.pitem.N > 0) produce<C>(&src_map, p, ring, full, queue, s);
+    }
+    if (tid == 0) {
+        Prod& pr = *prod_state<C>(full);
+        pr.ld_issued = 0;
+        pr.pq = pr.pn = 0;
+        next_item<C>(p, queue, pr);
+        while (pr.ld_issued < C::AHEAD && pr.pitem.N > 0) produce<C>(&src_map, p, ring, full, queue);
     }
     __syncthreads();
 
@@ -400,12 +449,14 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map, const JacobiParams
     s.cq = 0;
     s.it = queue[0];
     while (s.it.N > 0) {
+        item_output<C>(p, s);
         // FAST steps: every cell computed is interior -- the tile's rows and
         // columns lie inside [1,nj] x [1,ni] (per item) and all T planes the
         // levels compute at this step lie inside [1,nk] (per step: only the
         // first/last steps of items touching the k boundary are excluded)
+        const int jlo = s.it.J0 - (T - 1);  // the tile's first computed row
         const bool ij_in = (s.it.I0 - C::H >= 1) && (s.it.I0 - C::H + C::BW - 1 <= p.ni) &&
-                           (s.it.J0 - (T - 1) >= 1) && (s.it.J0 - (T - 1) + C::ROWS - 1 <= p.nj);
+                           (jlo >= 1) && (jlo + C::ROWS - 1 <= p.nj);
         // step n computes planes kb-T+n-L for L = 1..T
         const int n_lo = ij_in ? min(s.it.N, max(0, 2 * T + 1 - s.it.kb)) : s.it.N;
         const int n_hi = ij_in ? max(n_lo, min(s.it.N, p.nk + 2 + T - s.it.kb)) : s.it.N;

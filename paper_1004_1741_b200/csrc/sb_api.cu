@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -217,6 +218,7 @@ static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk
         int o = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::NT, C::SMEM_BYTES);
         if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
+        o *= sms;  // CTAs on the device
         if (o < 1) return fail(SB_ERR_CUDA, "jacobi T=%d kernel does not fit on an SM", C::T);
         occ = o;
     }
@@ -230,7 +232,7 @@ static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk
     p.nk = nk;
     p.tiles_i = (ni + 1 + C::TO - 1) / C::TO;  // tiles [TO*t, TO*t+TO) must cover [1, ni]
     p.tiles_j = (nj + C::TJ - 1) / C::TJ;
-    const int grid = sms * occ;
+    const int grid = occ;  // resident CTAs
     const int tiles = p.tiles_i * p.tiles_j;
     // k-block: aim for ~8 items per CTA, but never shorter than 8T planes
     // (each item re-reads 2T halo planes)
@@ -248,10 +250,10 @@ static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk
     p.b = b;
     p.counter = counters;
     p.dst = dst;
+    p.plane = nip * njp;
     cudaError_t e = cudaMemsetAsync(counters, 0, sizeof(int), st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counter)");
-    const int nctas = min(grid, p.items);
-    kern<<<nctas, C::NT, C::SMEM_BYTES, st>>>(smap, p);
+    kern<<<min(grid, p.items), C::NT, C::SMEM_BYTES, st>>>(smap, p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "jacobi_tb launch");
     return SB_OK;
@@ -325,7 +327,9 @@ int check_dims(int64_t ni, int64_t nj, int64_t nk) {
         return fail(SB_ERR_DIMENSION, "extents must be positive, got %lldx%lldx%lld",
                     (long long)ni, (long long)nj, (long long)nk);
     // int32 indexing inside kernels and TMA coordinates
+    // (plane offsets are 32-bit: (ni+2)(nj+2) < 2^31)
     if (ni > (1 << 20) || nj > (1 << 20) || nk > (1 << 20) ||
+        (ni + 2) * (nj + 2) >= (int64_t(1) << 31) ||
         (ni + 2) * (nj + 2) * (nk + 2) > (int64_t(1) << 40))
         return fail(SB_ERR_DIMENSION, "grid %lldx%lldx%lld too large", (long long)ni,
                     (long long)nj, (long long)nk);
@@ -352,6 +356,12 @@ int jacobi_block(const double* src, double* dst, int ni, int nj, int nk, int kfi
     return launch_generic(src, dst, ni, nj, kfirst, klast, a, b, st);
 }
 
+// Deepest fused launch worth running on a full domain: beyond T = 4 the
+// trapezoid overlap (and the register queues) cost more than the HBM
+// traffic saved, so deeper requests run as back-to-back 4-sweep launches
+// (bit-identical: the depth is a schedule, not part of the arithmetic).
+constexpr int kMaxFusedDepth = 4;
+
 // Advance `iters` Jacobi sweeps between two device buffers whose halos are
 // already equal.  Returns through *in_b whether the result is in `b_buf`.
 int jacobi_run(double* a_buf, double* b_buf, int ni, int nj, int nk, int64_t iters, double a,
@@ -360,6 +370,7 @@ int jacobi_run(double* a_buf, double* b_buf, int ni, int nj, int nk, int64_t ite
     double* src = a_buf;
     double* dst = b_buf;
     int64_t left = iters;
+    depth = std::min(depth, kMaxFusedDepth);
     while (left > 0) {
         int T = (int)((left >= depth) ? depth : left);
         if (!tma) T = 1;
