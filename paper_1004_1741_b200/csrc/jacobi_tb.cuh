@@ -158,6 +158,7 @@ struct JState {      // per-thread loop state shared by the step functions
     ItemInfo it;     // current item
     uint32_t ooff;   // this thread's output cell (row 0) within a plane
     uint32_t omask;  // bit r: row r of this thread is an output row of the current item
+    uint32_t keep0, keep1;  // bit r: cell 0 / 1 of row r is a Dirichlet cell (SEL steps)
 };
 
 // The TMA producer's state.  Only thread 0 produces, so it lives in shared
@@ -184,6 +185,13 @@ __device__ __forceinline__ void item_output(const JacobiParams& p, JState& s) {
     }
     s.omask = m;
     s.ooff = uint32_t(gj * (p.ni + 2) + gi);
+    uint32_t rows_out = 0;
+#pragma unroll
+    for (int r = 0; r < C::RJ; ++r)
+        if (gj + r < 1 || gj + r > p.nj) rows_out |= 1u << r;
+    const uint32_t all = (1u << C::RJ) - 1;
+    s.keep0 = rows_out | ((gi >= 1 && gi <= p.ni) ? 0u : all);
+    s.keep1 = rows_out | ((gi + 1 >= 1 && gi + 1 <= p.ni) ? 0u : all);
 }
 
 // The producer's next work item.
@@ -216,15 +224,23 @@ __device__ __forceinline__ void produce(const CUtensorMap* src_map, const Jacobi
     }
 }
 
+// Step modes.  FAST: every cell the tile computes at this step is interior.
+// SEL: the planes are interior but the tile touches the i/j boundary: the
+// FAST arithmetic, then Dirichlet cells keep their value (per-item masks).
+// SLOW: anything (k-boundary steps, tiny grids): full predication, and rows
+// outside a level's trapezoid skip their arithmetic.
+enum StepMode { SLOW = 0, FAST = 1, SEL = 2 };
+
 // One level's update of a thread's RJ rows x 2 cells.  cen: the centre
 // plane with the south (row 0) and north (row RJ+1) neighbour rows; dn/up:
 // the planes below and above.
-template <class C, bool FAST, bool AZ>
+template <class C, int MODE, bool AZ>
 __device__ __forceinline__ void level_update(const double (&cen)[C::RJ + 2][2],
                                              const double (&dn)[C::RJ][2],
                                              const double (&up)[C::RJ][2], double (&nv)[C::RJ][2],
                                              double a, double b, int L, int dj, int k, int gj,
-                                             bool in_i0, bool in_i1, const JacobiParams& p) {
+                                             bool in_i0, bool in_i1, const JacobiParams& p,
+                                             const JState& s) {
     constexpr int T = C::T, RJ = C::RJ;
 #pragma unroll
     for (int r = 0; r < RJ; ++r) {
@@ -232,7 +248,7 @@ __device__ __forceinline__ void level_update(const double (&cen)[C::RJ + 2][2],
         const double wv = __shfl_up_sync(0xffffffffu, c1, 1);    // cell i-1 (lane-1)
         const double ev = __shfl_down_sync(0xffffffffu, c0, 1);  // cell i+2 (lane+1)
         bool compute = true;
-        if (!FAST) {
+        if (MODE == SLOW) {
             const int jr = dj + r, need = T - L;
             compute = (jr >= -need) && (jr < C::TJ + need) && (k >= 1) && (k <= p.nk) &&
                       (gj + r >= 1) && (gj + r <= p.nj);
@@ -249,9 +265,12 @@ __device__ __forceinline__ void level_update(const double (&cen)[C::RJ + 2][2],
             acc1 = __dadd_rn(acc1, up[r][1]);
             const double o0 = jac_final<AZ>(a, b, c0, acc0);
             const double o1 = jac_final<AZ>(a, b, c1, acc1);
-            if (FAST) {
+            if (MODE == FAST) {
                 nv[r][0] = o0;
                 nv[r][1] = o1;
+            } else if (MODE == SEL) {
+                nv[r][0] = (s.keep0 & (1u << r)) ? c0 : o0;
+                nv[r][1] = (s.keep1 & (1u << r)) ? c1 : o1;
             } else {
                 nv[r][0] = in_i0 ? o0 : c0;
                 nv[r][1] = in_i1 ? o1 : c1;
@@ -263,12 +282,10 @@ __device__ __forceinline__ void level_update(const double (&cen)[C::RJ + 2][2],
     }
 }
 
-// One plane step of the current item.  FAST: every cell the tile computes
-// this item is interior (no Dirichlet masks, no trapezoid row skipping).
-// PH = g mod 3 selects the register rotation statically.  With C::L1S level
+// One plane step of the current item in StepMode MODE.  PH = g mod 3 selects the register rotation statically.  With C::L1S level
 // 1 reads its three input planes straight from the TMA ring (slots g-2,
 // g-1, g); otherwise from register queue Q[0], fed from ring slot g.
-template <class C, bool FAST, bool AZ, int PH>
+template <class C, int MODE, bool AZ, int PH>
 __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const JacobiParams& p,
                                             double* ring, double* xb, uint64_t* full,
                                             ItemInfo* queue, LevelQ<C> (&Q)[C::NQ],
@@ -325,7 +342,7 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
                 up[r][0] = y.x;
                 up[r][1] = y.y;
             }
-            level_update<C, FAST, AZ>(cen, dn, up, nv, a, b, L, dj, k, gj, in_i0, in_i1, p);
+            level_update<C, MODE, AZ>(cen, dn, up, nv, a, b, L, dj, k, gj, in_i0, in_i1, p, s);
         } else {
             LevelQ<C>& In = Q[C::L1S ? L - 2 : L - 1];
             double2 s2, n2;
@@ -350,8 +367,8 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
                 cen[r + 1][0] = In.q[CC][r][0];
                 cen[r + 1][1] = In.q[CC][r][1];
             }
-            level_update<C, FAST, AZ>(cen, In.q[D], In.q[U], nv, a, b, L, dj, k, gj, in_i0, in_i1,
-                                      p);
+            level_update<C, MODE, AZ>(cen, In.q[D], In.q[U], nv, a, b, L, dj, k, gj, in_i0, in_i1,
+                                      p, s);
         }
         if (L < T) {
             double* xl = xb + size_t((L - 1) * C::XB + xwb) * C::XSLOT * C::XROW;
@@ -381,9 +398,9 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
     return ++s.n == it.N;
 }
 
-// `count` plane steps of the current item (all of them FAST or not),
+// `count` plane steps of the current item (all in one StepMode),
 // entering the 3-phase register rotation at g mod 3.
-template <class C, bool FAST, bool AZ>
+template <class C, int MODE, bool AZ>
 __device__ __forceinline__ void jacobi_steps(const CUtensorMap* src_map, const JacobiParams& p,
                                              double* ring, double* xb, uint64_t* full,
                                              ItemInfo* queue, LevelQ<C> (&Q)[C::NQ],
@@ -391,20 +408,20 @@ __device__ __forceinline__ void jacobi_steps(const CUtensorMap* src_map, const J
     if (count <= 0) return;
     const int ph = s.g % 3;
     if (ph == 1) {
-        jacobi_step<C, FAST, AZ, 1>(src_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 1>(src_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
-        jacobi_step<C, FAST, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
     } else if (ph == 2) {
-        jacobi_step<C, FAST, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
     }
     while (true) {
-        jacobi_step<C, FAST, AZ, 0>(src_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 0>(src_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
-        jacobi_step<C, FAST, AZ, 1>(src_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 1>(src_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
-        jacobi_step<C, FAST, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
     }
 }
@@ -450,19 +467,21 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map, const JacobiParams
     s.it = queue[0];
     while (s.it.N > 0) {
         item_output<C>(p, s);
-        // FAST steps: every cell computed is interior -- the tile's rows and
-        // columns lie inside [1,nj] x [1,ni] (per item) and all T planes the
-        // levels compute at this step lie inside [1,nk] (per step: only the
-        // first/last steps of items touching the k boundary are excluded)
+        // Steps [n_lo, n_hi) compute interior planes only (step n computes
+        // planes kb-T+n-L for L = 1..T; only the first/last steps of items
+        // touching the k boundary are outside).  They run FAST when the
+        // tile's rows and columns lie inside [1,nj] x [1,ni], else SEL.
         const int jlo = s.it.J0 - (T - 1);  // the tile's first computed row
         const bool ij_in = (s.it.I0 - C::H >= 1) && (s.it.I0 - C::H + C::BW - 1 <= p.ni) &&
                            (jlo >= 1) && (jlo + C::ROWS - 1 <= p.nj);
-        // step n computes planes kb-T+n-L for L = 1..T
-        const int n_lo = ij_in ? min(s.it.N, max(0, 2 * T + 1 - s.it.kb)) : s.it.N;
-        const int n_hi = ij_in ? max(n_lo, min(s.it.N, p.nk + 2 + T - s.it.kb)) : s.it.N;
-        jacobi_steps<C, false, AZ>(&src_map, p, ring, xb, full, queue, Q, s, n_lo);
-        jacobi_steps<C, true, AZ>(&src_map, p, ring, xb, full, queue, Q, s, n_hi - n_lo);
-        jacobi_steps<C, false, AZ>(&src_map, p, ring, xb, full, queue, Q, s, s.it.N - n_hi);
+        const int n_lo = min(s.it.N, max(0, 2 * T + 1 - s.it.kb));
+        const int n_hi = max(n_lo, min(s.it.N, p.nk + 2 + T - s.it.kb));
+        jacobi_steps<C, SLOW, AZ>(&src_map, p, ring, xb, full, queue, Q, s, n_lo);
+        if (ij_in)
+            jacobi_steps<C, FAST, AZ>(&src_map, p, ring, xb, full, queue, Q, s, n_hi - n_lo);
+        else
+            jacobi_steps<C, SEL, AZ>(&src_map, p, ring, xb, full, queue, Q, s, n_hi - n_lo);
+        jacobi_steps<C, SLOW, AZ>(&src_map, p, ring, xb, full, queue, Q, s, s.it.N - n_hi);
         s.n = 0;
         __syncthreads();  // queue[] entry written by thread 0 at least one barrier ago
         s.cq = (s.cq + 1) % C::QSLOTS;
