@@ -21,7 +21,11 @@
 //     registers -- for level 1 optionally not: it can read the TMA ring
 //     directly (JacobiCfg::L1S); levels trail by one plane, one
 //     __syncthreads per plane;
-//   * output rows leave with coalesced 16-byte global stores.
+//   * level T stages its output tile in shared memory and one thread writes
+//     it with a TMA tensor store per plane (JacobiCfg::TS; the per-thread
+//     alternative, coalesced 16-byte global stores, cost ~70 address
+//     instructions per step that the compiler rematerialised under register
+//     pressure).
 // Overlapped (trapezoid) tiling: level L is valid on the tile grown by T-L
 // cells; rows outside that region skip their arithmetic.
 //
@@ -60,9 +64,13 @@ struct JacobiParams {
     int64_t plane;           // (nj + 2) * (ni + 2) cells, < 2^31 (check_dims)
 };
 
-template <int T_, int RJ_, int NW_, int S_, int MINB_, bool L1S_ = false>
+template <int T_, int RJ_, int NW_, int S_, int MINB_, bool L1S_ = false, bool TS_ = false>
 struct JacobiCfg {
     static constexpr int T = T_, RJ = RJ_, NW = NW_, S = S_, MINB = MINB_;
+    // TS: level T writes its output tile into a shared staging buffer (double
+    // buffered) and one thread stores it with a TMA tensor store per plane,
+    // instead of per-thread 16-byte global stores
+    static constexpr bool TS = TS_;
     // L1S: level 1 reads planes k-1, k, k+1 from the ring (three live slots,
     // prefetch distance S-2) instead of a register queue (prefetch S-1):
     // fewer registers (more warps / CTAs per SM), more shared-memory loads
@@ -90,7 +98,9 @@ struct JacobiCfg {
     static constexpr int QSLOTS = 4;
     static constexpr size_t RING_OFF = 0;
     static constexpr size_t X_OFF = RING_OFF + size_t(S) * BOXS;
-    static constexpr size_t DBL_END = X_OFF + size_t(NX) * XB * XSLOT * XROW;
+    static constexpr int STG = (TO * TJ + 15) / 16 * 16;  // staging doubles per buffer
+    static constexpr size_t STG_OFF = X_OFF + size_t(NX) * XB * XSLOT * XROW;
+    static constexpr size_t DBL_END = STG_OFF + (TS ? 2 * size_t(STG) : 0);
     // doubles, then queue[QSLOTS], mbarriers full[S], then the producer state
     static constexpr size_t SMEM_BYTES = DBL_END * 8 + 16 * QSLOTS + 8 * S + 32 + 64;
     static constexpr uint32_t BOX_BYTES = uint32_t(BOX) * 8;
@@ -159,6 +169,8 @@ struct JState {      // per-thread loop state shared by the step functions
     uint32_t ooff;   // this thread's output cell (row 0) within a plane
     uint32_t omask;  // bit r: row r of this thread is an output row of the current item
     uint32_t keep0, keep1;  // bit r: cell 0 / 1 of row r is a Dirichlet cell (SEL steps)
+    uint32_t smask;  // TS: bit r: row r of this thread lies in the staged output tile
+    int soff;        // TS: staging offset of this thread's row 0
 };
 
 // The TMA producer's state.  Only thread 0 produces, so it lives in shared
@@ -177,14 +189,16 @@ __device__ __forceinline__ void item_output(const JacobiParams& p, JState& s) {
     const int di = 2 * lane - C::H;
     const int dj = -(C::T - 1) + w * C::RJ;
     const int gi = s.it.I0 + di, gj = s.it.J0 + dj;
-    uint32_t m = 0;
-    if (di >= 0 && di < C::TO && gi + 1 <= p.ni + 1) {
+    if (!C::TS) {
+        uint32_t m = 0;
+        if (di >= 0 && di < C::TO && gi + 1 <= p.ni + 1) {
 #pragma unroll
-        for (int r = 0; r < C::RJ; ++r)
-            if (dj + r >= 0 && dj + r < C::TJ && gj + r <= p.nj) m |= 1u << r;
+            for (int r = 0; r < C::RJ; ++r)
+                if (dj + r >= 0 && dj + r < C::TJ && gj + r <= p.nj) m |= 1u << r;
+        }
+        s.omask = m;
+        s.ooff = uint32_t(gj * (p.ni + 2) + gi);
     }
-    s.omask = m;
-    s.ooff = uint32_t(gj * (p.ni + 2) + gi);
     uint32_t rows_out = 0;
 #pragma unroll
     for (int r = 0; r < C::RJ; ++r)
@@ -286,7 +300,8 @@ __device__ __forceinline__ void level_update(const double (&cen)[C::RJ + 2][2],
 // 1 reads its three input planes straight from the TMA ring (slots g-2,
 // g-1, g); otherwise from register queue Q[0], fed from ring slot g.
 template <class C, int MODE, bool AZ, int PH>
-__device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const JacobiParams& p,
+__device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CUtensorMap* dst_map,
+                                            const JacobiParams& p,
                                             double* ring, double* xb, uint64_t* full,
                                             ItemInfo* queue, LevelQ<C> (&Q)[C::NQ],
                                             JState& s) {
@@ -380,6 +395,13 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
                 Q[C::L1S ? L - 1 : L].q[U][r][0] = nv[r][0];
                 Q[C::L1S ? L - 1 : L].q[U][r][1] = nv[r][1];
             }
+        } else if (C::TS) {
+            if (s.n >= 2 * T && s.smask) {
+                double* stg = ring + C::STG_OFF + (s.g & 1) * C::STG;
+#pragma unroll
+                for (int r = 0; r < RJ; ++r)
+                    if (s.smask & (1u << r)) sts2(stg + s.soff + r * C::TO, nv[r][0], nv[r][1]);
+            }
         } else if (s.n >= 2 * T && s.omask) {
             double* plane = p.dst + (int64_t)k * p.plane;  // CTA-uniform
             uint32_t o = s.ooff;
@@ -391,9 +413,23 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
             }
         }
     }
+    const bool out_step = s.n >= 2 * T;
+    if (C::TS && out_step) {
+        fence_proxy_async_smem();  // staged rows -> visible to the TMA store
+        // the store issued last step has read the other staging buffer, which
+        // the next step overwrites
+        if (tid == 0) bulk_wait_read<0>();
+    }
     __syncthreads();
-    // the oldest ring slot (g-2 with L1S, else g-1) is free now: refill it
-    if (tid == 0) produce<C>(src_map, p, ring, full, queue);
+    if (tid == 0) {
+        if (C::TS && out_step) {
+            tma_store_3d(dst_map, ring + C::STG_OFF + (s.g & 1) * C::STG, it.I0, it.J0,
+                         it.kb - 2 * T + s.n);
+            bulk_commit();
+        }
+        // the oldest ring slot (g-2 with L1S, else g-1) is free now: refill it
+        produce<C>(src_map, p, ring, full, queue);
+    }
     ++s.g;
     return ++s.n == it.N;
 }
@@ -401,34 +437,36 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const Ja
 // `count` plane steps of the current item (all in one StepMode),
 // entering the 3-phase register rotation at g mod 3.
 template <class C, int MODE, bool AZ>
-__device__ __forceinline__ void jacobi_steps(const CUtensorMap* src_map, const JacobiParams& p,
+__device__ __forceinline__ void jacobi_steps(const CUtensorMap* src_map, const CUtensorMap* dst_map,
+                                             const JacobiParams& p,
                                              double* ring, double* xb, uint64_t* full,
                                              ItemInfo* queue, LevelQ<C> (&Q)[C::NQ],
                                              JState& s, int count) {
     if (count <= 0) return;
     const int ph = s.g % 3;
     if (ph == 1) {
-        jacobi_step<C, MODE, AZ, 1>(src_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 1>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
-        jacobi_step<C, MODE, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 2>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
     } else if (ph == 2) {
-        jacobi_step<C, MODE, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 2>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
     }
     while (true) {
-        jacobi_step<C, MODE, AZ, 0>(src_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 0>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
-        jacobi_step<C, MODE, AZ, 1>(src_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 1>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
-        jacobi_step<C, MODE, AZ, 2>(src_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 2>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
     }
 }
 
 template <class C, bool AZ>
 __global__ void __launch_bounds__(C::NT, C::MINB)
-jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map, const JacobiParams p) {
+jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
+                 const __grid_constant__ CUtensorMap dst_map, const JacobiParams p) {
     constexpr int T = C::T, S = C::S;
     extern __shared__ __align__(128) double smem[];
     double* ring = smem + C::RING_OFF;
@@ -441,6 +479,7 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map, const JacobiParams
     JState s;
     if (tid == 0) {
         tma_prefetch_desc(&src_map);
+        if (C::TS) tma_prefetch_desc(&dst_map);
         for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
         fence_mbar_init();
     }
@@ -465,6 +504,18 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map, const JacobiParams
     s.n = 0;
     s.cq = 0;
     s.it = queue[0];
+    if (C::TS) {  // this thread's cells in the staged TO x TJ output tile (item-invariant)
+        const int lane = tid & 31, w = tid >> 5;
+        const int di = 2 * lane - C::H, dj = -(T - 1) + w * C::RJ;
+        uint32_t m = 0;
+        if (di >= 0 && di < C::TO) {
+#pragma unroll
+            for (int r = 0; r < C::RJ; ++r)
+                if (dj + r >= 0 && dj + r < C::TJ) m |= 1u << r;
+        }
+        s.smask = m;
+        s.soff = dj * C::TO + di;
+    }
     while (s.it.N > 0) {
         item_output<C>(p, s);
         // Steps [n_lo, n_hi) compute interior planes only (step n computes
@@ -476,17 +527,18 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map, const JacobiParams
                            (jlo >= 1) && (jlo + C::ROWS - 1 <= p.nj);
         const int n_lo = min(s.it.N, max(0, 2 * T + 1 - s.it.kb));
         const int n_hi = max(n_lo, min(s.it.N, p.nk + 2 + T - s.it.kb));
-        jacobi_steps<C, SLOW, AZ>(&src_map, p, ring, xb, full, queue, Q, s, n_lo);
+        jacobi_steps<C, SLOW, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, n_lo);
         if (ij_in)
-            jacobi_steps<C, FAST, AZ>(&src_map, p, ring, xb, full, queue, Q, s, n_hi - n_lo);
+            jacobi_steps<C, FAST, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, n_hi - n_lo);
         else
-            jacobi_steps<C, SEL, AZ>(&src_map, p, ring, xb, full, queue, Q, s, n_hi - n_lo);
-        jacobi_steps<C, SLOW, AZ>(&src_map, p, ring, xb, full, queue, Q, s, s.it.N - n_hi);
+            jacobi_steps<C, SEL, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, n_hi - n_lo);
+        jacobi_steps<C, SLOW, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, s.it.N - n_hi);
         s.n = 0;
         __syncthreads();  // queue[] entry written by thread 0 at least one barrier ago
         s.cq = (s.cq + 1) % C::QSLOTS;
         s.it = queue[s.cq];
     }
+    if (C::TS && tid == 0) bulk_wait<0>();  // every output plane written before exit
 }
 
 }  // namespace sb

@@ -222,9 +222,14 @@ static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk
         if (o < 1) return fail(SB_ERR_CUDA, "jacobi T=%d kernel does not fit on an SM", C::T);
         occ = o;
     }
-    CUtensorMap smap;
+    CUtensorMap smap, dmap;
     const int64_t nip = ni + 2, njp = nj + 2, nkp = nk + 2;
     if ((rc = make_grid_map(&smap, src, nip, njp, nkp, C::BW, C::BH))) return rc;
+    if (C::TS) {
+        if ((rc = make_grid_map(&dmap, dst, nip, njp, nkp, C::TO, C::TJ))) return rc;
+    } else {
+        dmap = smap;  // unused
+    }
 
     JacobiParams p;
     p.ni = ni;
@@ -253,7 +258,7 @@ static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk
     p.plane = nip * njp;
     cudaError_t e = cudaMemsetAsync(counters, 0, sizeof(int), st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counter)");
-    kern<<<min(grid, p.items), C::NT, C::SMEM_BYTES, st>>>(smap, p);
+    kern<<<min(grid, p.items), C::NT, C::SMEM_BYTES, st>>>(smap, dmap, p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "jacobi_tb launch");
     return SB_OK;
@@ -267,7 +272,8 @@ static int launch_tb(const double* src, double* dst, int ni, int nj, int nk, int
     return launch_tb_impl<C, false>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
 }
 
-// tile configurations per depth: <T, RJ rows/thread, NW warps, S ring stages, MINB>
+// tile configurations per depth: <T, RJ rows/thread, NW warps, S ring stages, MINB,
+// L1S level 1 from the ring, TS TMA-store output>
 // (SB_JCFG=<variant> selects alternatives during tuning)
 static int jcfg_variant() {
     static int v = getenv("SB_JCFG") ? atoi(getenv("SB_JCFG")) : 0;
@@ -282,7 +288,8 @@ static int launch_depth(int T, const double* src, double* dst, int ni, int nj, i
     switch (T) {
         case 1:
             if (v == 1) SB_L(1, 2, 8, 4, 4);
-            SB_L(1, 4, 8, 4, 2);
+            if (v == 4) SB_L(1, 4, 8, 4, 2);
+            SB_L(1, 4, 8, 4, 2, false, true);
         case 2:
             if (v == 1) SB_L(2, 4, 8, 4, 2);
             if (v == 2) SB_L(2, 4, 12, 5, 1, true);
@@ -291,12 +298,14 @@ static int launch_depth(int T, const double* src, double* dst, int ni, int nj, i
             if (v == 1) SB_L(3, 2, 16, 4, 1);
             if (v == 2) SB_L(3, 3, 16, 5, 1, true);
             if (v == 3) SB_L(3, 4, 8, 4, 2, true);
-            SB_L(3, 4, 12, 5, 1, true);
+            if (v == 4) SB_L(3, 4, 12, 5, 1, true);
+            SB_L(3, 4, 12, 5, 1, true, true);
         case 4:
             if (v == 1) SB_L(4, 2, 16, 4, 1);
             if (v == 2) SB_L(4, 4, 12, 5, 1, true);
             if (v == 3) SB_L(4, 3, 16, 5, 1, true);
-            SB_L(4, 4, 8, 4, 1);
+            if (v == 4) SB_L(4, 4, 8, 4, 1);
+            SB_L(4, 4, 8, 4, 1, false, true);
         case 5: SB_L(5, 2, 12, 3, 1);
         case 6: SB_L(6, 2, 12, 3, 1);
         case 7: SB_L(7, 2, 12, 3, 1);
