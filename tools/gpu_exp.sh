@@ -1,3 +1,6 @@
 cd $GRAFT_REPO_ROOT
-echo "single, cluster-2 launch"; SB_FORCE_CLUSTER=1 timeout 300 python tools/probe.py --n 1024 --iters 12 --depths 1,3,4 --reps 2 2>&1 | tail -3
-echo "single"; timeout 300 python tools/probe.py --n 1024 --iters 12 --depths 1,3,4 --reps 2 2>&1 | tail -3
+for rep in 1 2; do
+timeout 300 python tools/probe.py --n 1024 --iters 12 --depths 3 --reps 3 2>&1 | tail -1 | sed "s/^/auto-alone /"
+SB_KBLK=395 timeout 300 python tools/probe.py --n 1024 --iters 12 --depths 3 --reps 3 2>&1 | tail -1 | sed "s/^/kb395 /"
+timeout 300 python tools/probe.py --n 1024 --iters 12 --depths 2,3 --reps 3 2>&1 | tail -1 | sed "s/^/auto-after-T2 /"
+done
