@@ -147,6 +147,20 @@ int sb_run_host(int kernel, double* host_grid, int64_t ni, int64_t nj, int64_t n
                 int64_t iters, double a, double b, int depth, int device);
 
 /*
+ * Batch form of sb_run_host for a stream of independent grids of one shape
+ * (the reference's perf.measure runs fresh inputs back to back): entry i's
+ * host->device copy overlaps entry i-1's sweeps and entry i-2's
+ * device->host copy, so with pinned grids the batch moves at
+ * max(H2D, sweeps, D2H) per grid.  Entries are processed in order; an entry
+ * may repeat the pointer of an entry at least two places earlier and then
+ * starts from that entry's result; adjacent repeats -> SB_ERR_ARGUMENT.
+ * Synchronous; every grid is updated in place.  Uses two device slots
+ * (Jacobi: four grids' worth of device memory).
+ */
+int sb_run_host_batch(int kernel, double* const* host_grids, int count, int64_t ni, int64_t nj,
+                      int64_t nk, int64_t iters, double a, double b, int depth, int device);
+
+/*
  * Device bandwidth probe: a[i] = b[i] + s*c[i] for n doubles (device
  * pointers, 16-byte aligned), the STREAM triad of the reference's
  * perf.stream_triad (pkg/src/stencilbench/perf.py:139-211) on the GPU.

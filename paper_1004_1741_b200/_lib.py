@@ -45,6 +45,7 @@ SIGNATURES = {
     "sb_reference_sweeps": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _dbl, _dbl, _vp,
                                    ctypes.POINTER(_int)]),
     "sb_run_host": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _dbl, _dbl, _int, _int]),
+    "sb_run_host_batch": (_int, [_int, _vp, _int, _i64, _i64, _i64, _i64, _dbl, _dbl, _int, _int]),
     "sb_triad": (_int, [_vp, _vp, _vp, _dbl, _i64, _vp]),
     "sb_host_alloc": (_vp, [_i64]),
     "sb_host_free": (None, [_vp]),

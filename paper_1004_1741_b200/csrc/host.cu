@@ -108,6 +108,121 @@ int sb_run_host(int kernel, double* host_grid, int64_t ni, int64_t nj, int64_t n
     return SB_OK;
 }
 
+// Pipelined host-buffer batch: entry i's upload overlaps entry i-1's sweeps
+// and entry i-2's download (two device slots, one stream each for H2D,
+// sweeps and D2H; PCIe is full duplex and the copy engines are separate), so
+// a stream of grids moves at max(H2D, sweeps, D2H) per grid instead of the
+// sum.  Ordering: D2H(i) completes before H2D(i+2) starts (same slot), so an
+// entry may repeat the pointer of an entry >= 2 places earlier and then starts
+// from that entry's result; adjacent repeats are rejected.
+struct BatchCtx {
+    double* g[2] = {nullptr, nullptr};
+    double* s[2] = {nullptr, nullptr};
+    size_t cap = 0;
+    bool two = false;
+    cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // H2D, sweeps, D2H
+    cudaEvent_t up[2], done[2], down[2];
+    bool ev = false;
+};
+static BatchCtx g_batch[64];
+
+static void batch_free(BatchCtx& B) {
+    for (int i = 0; i < 2; ++i) {
+        if (B.g[i]) cudaFree(B.g[i]);
+        if (B.s[i]) cudaFree(B.s[i]);
+        B.g[i] = B.s[i] = nullptr;
+    }
+    B.cap = 0;
+}
+
+int sb_run_host_batch(int kernel, double* const* host_grids, int count, int64_t ni, int64_t nj,
+                      int64_t nk, int64_t iters, double a, double b, int depth, int device) {
+    clear_error();
+    int rc = check_dims(ni, nj, nk);
+    if (rc) return rc;
+    if (iters < 0) return fail(SB_ERR_PLAN, "iter_end must be >= 0, got %lld", (long long)iters);
+    if (kernel < SB_KERNEL_JACOBI || kernel > SB_KERNEL_GS_INTERLEAVED)
+        return fail(SB_ERR_PLAN, "unknown kernel %d", kernel);
+    if (kernel == SB_KERNEL_JACOBI && (depth < 1 || depth > sb_max_depth()))
+        return fail(SB_ERR_PLAN, "depth must be in [1, %d], got %d", sb_max_depth(), depth);
+    if (count < 0 || (count > 0 && !host_grids)) return fail(SB_ERR_ARGUMENT, "bad grid list");
+    for (int i = 0; i < count; ++i) {
+        if (!host_grids[i]) return fail(SB_ERR_ARGUMENT, "null grid pointer at %d", i);
+        if (i > 0 && host_grids[i] == host_grids[i - 1])
+            return fail(SB_ERR_ARGUMENT, "entries %d and %d are the same grid", i - 1, i);
+    }
+    if (iters == 0 || count == 0) return SB_OK;
+    int ndev = sb_device_count();
+    if (ndev < 1) return fail(SB_ERR_NODEVICE, "no CUDA device");
+    if (device < 0 || device >= ndev || device >= 64)
+        return fail(SB_ERR_ARGUMENT, "device %d out of range (%d visible)", device, ndev);
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    BatchCtx& B = g_batch[device];
+    const size_t cells = size_t(ni + 2) * size_t(nj + 2) * size_t(nk + 2);
+    const size_t bytes = cells * sizeof(double);
+    const bool two = (kernel == SB_KERNEL_JACOBI);
+    if (!B.st[0]) {
+        for (int i = 0; i < 3; ++i)
+            if ((e = cudaStreamCreateWithFlags(&B.st[i], cudaStreamNonBlocking)) != cudaSuccess)
+                return cuda_fail(e, "cudaStreamCreate");
+    }
+    if (!B.ev) {
+        for (int i = 0; i < 2; ++i) {
+            if ((e = cudaEventCreateWithFlags(&B.up[i], cudaEventDisableTiming)) != cudaSuccess ||
+                (e = cudaEventCreateWithFlags(&B.done[i], cudaEventDisableTiming)) != cudaSuccess ||
+                (e = cudaEventCreateWithFlags(&B.down[i], cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(e, "cudaEventCreate");
+        }
+        B.ev = true;
+    }
+    if (B.cap < cells || (two && !B.two)) {
+        batch_free(B);
+        for (int i = 0; i < 2; ++i) {
+            if ((e = cudaMalloc(&B.g[i], bytes)) != cudaSuccess ||
+                (two && (e = cudaMalloc(&B.s[i], bytes)) != cudaSuccess)) {
+                batch_free(B);
+                return cuda_fail(e, "cudaMalloc(batch slots)");
+            }
+        }
+        B.cap = cells;
+        B.two = two;
+    }
+    cudaStream_t h2d = B.st[0], comp = B.st[1], d2h = B.st[2];
+    for (int i = 0; i < count; ++i) {
+        const int sl = i & 1;
+        if (i >= 2 && (e = cudaStreamWaitEvent(h2d, B.down[sl], 0)) != cudaSuccess)
+            return cuda_fail(e, "cudaStreamWaitEvent");
+        if ((e = cudaMemcpyAsync(B.g[sl], host_grids[i], bytes, cudaMemcpyHostToDevice, h2d)) !=
+                cudaSuccess ||
+            (e = cudaEventRecord(B.up[sl], h2d)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(comp, B.up[sl], 0)) != cudaSuccess)
+            return cuda_fail(e, "H2D copy");
+        const double* result = B.g[sl];
+        if (two) {
+            int in_s = 0;
+            rc = sb_jacobi(B.g[sl], B.s[sl], ni, nj, nk, iters, a, b, depth, comp, &in_s);
+            if (rc) return rc;
+            result = in_s ? B.s[sl] : B.g[sl];
+        } else {
+            rc = sb_gs(B.g[sl], ni, nj, nk, iters, b, kernel, comp);
+            if (rc) return rc;
+        }
+        if ((e = cudaEventRecord(B.done[sl], comp)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(d2h, B.done[sl], 0)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(host_grids[i], result, bytes, cudaMemcpyDeviceToHost, d2h)) !=
+                cudaSuccess ||
+            (e = cudaEventRecord(B.down[sl], d2h)) != cudaSuccess)
+            return cuda_fail(e, "D2H copy");
+    }
+    if ((e = cudaStreamSynchronize(d2h)) != cudaSuccess) return cuda_fail(e, "batch execution");
+    if ((e = cudaStreamSynchronize(comp)) != cudaSuccess) return cuda_fail(e, "batch execution");
+    if (!two) return gs_check_error(comp);
+    return SB_OK;
+}
+
 int sb_jacobi_planes(const double* src, double* dst, int64_t ni, int64_t nj, int64_t nk,
                      int64_t k_out_lo, int64_t k_out_hi, int sweeps, double a, double b,
                      void* stream) {

@@ -6,6 +6,7 @@ from .engine import (
     execute,
     resolve_depth,
     run,
+    run_batch,
     run_pipeline_gs,
     run_serial,
     run_threaded_jacobi,
@@ -27,7 +28,7 @@ from .plan import (
 
 __all__ = [
     "BARRIER_AUTO", "DEFAULT_DEPTH", "PIPELINE", "SERIAL", "THREADED", "VARIANTS", "WAVEFRONT",
-    "SweepPlan", "WavefrontConfig", "execute", "partition_blocks", "resolve_depth", "run",
+    "SweepPlan", "WavefrontConfig", "execute", "partition_blocks", "resolve_depth", "run", "run_batch",
     "run_pipeline_gs", "run_serial", "run_threaded_jacobi", "run_wavefront", "run_wavefront_gs",
     "run_wavefront_jacobi",
 ]

@@ -192,3 +192,55 @@ def run(plan, g, placement=None, stats=None, instrument=False):
     if plan.variant == WAVEFRONT:
         return run_wavefront(plan, g, placement=placement, stats=stats, instrument=instrument)
     raise PlanError(f"unknown variant {plan.variant!r}")
+
+
+def _validate(plan, g):
+    """The checks `run(plan, g)` performs before any work (same exceptions)."""
+    if plan.variant in (THREADED, PIPELINE):
+        if plan.kernel == JACOBI:
+            if plan.variant == PIPELINE:
+                raise PlanError("pipeline engine applies to Gauss-Seidel kernels only")
+            if plan.threads > g.nk:
+                raise PartitionError(f"{plan.threads} threads cannot split nk={g.nk} planes")
+        elif plan.threads > g.nj:
+            raise PartitionError(f"{plan.threads} threads cannot split nj={g.nj} lines")
+    elif plan.variant == WAVEFRONT:
+        _wavefront_checks(plan, g)
+    elif plan.variant != SERIAL:
+        raise PlanError(f"unknown variant {plan.variant!r}")
+
+
+def run_batch(plan, grids, device=None):
+    """`run(plan, g)` for each host grid of `grids` (one shape, numpy data),
+    pipelined on one GPU through ``sb_run_host_batch``: grid i's upload
+    overlaps grid i-1's sweeps and grid i-2's download.  Grids are processed
+    in order and updated in place; every grid is validated first (same
+    exceptions as `run`, raised before any work).  Returns `grids`."""
+    grids = list(grids)
+    if not grids:
+        return grids
+    g0 = grids[0]
+    arrs = []
+    for g in grids:
+        _validate(plan, g)
+        if (g.ni, g.nj, g.nk) != (g0.ni, g0.nj, g0.nk):
+            raise ValueError("run_batch needs grids of one shape")
+        arr = g.data
+        if not (isinstance(arr, np.ndarray) and arr.dtype == np.float64 and arr.flags.c_contiguous
+                and arr.flags.writeable and arr.shape == g.shape_padded):
+            raise ValueError("run_batch needs writeable C-contiguous float64 host grids")
+        arrs.append(arr)
+    if plan.iter_end == 0:
+        return grids
+    lib = _lib.load()
+    _lib.require_device()
+    if device is None:
+        import torch
+
+        device = torch.cuda.current_device()
+    ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+    depth = resolve_depth(plan, g0)
+    _lib.check(lib.sb_run_host_batch(_lib.KERNEL_IDS[plan.kernel], ptrs, len(arrs), g0.ni, g0.nj,
+                                     g0.nk, plan.iter_end, plan.coeffs.a, plan.coeffs.b, depth,
+                                     device))
+    return grids

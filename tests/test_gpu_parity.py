@@ -24,7 +24,7 @@ def _need_gpu():
 from paper_1004_1741_b200 import _lib  # noqa: E402
 from paper_1004_1741_b200.grid import Grid3D  # noqa: E402
 from paper_1004_1741_b200.kernels import StencilCoeffs  # noqa: E402
-from paper_1004_1741_b200.sweeps import SweepPlan, WavefrontConfig, execute, run  # noqa: E402
+from paper_1004_1741_b200.sweeps import SweepPlan, WavefrontConfig, execute, run, run_batch  # noqa: E402
 
 
 def run_device(kernel, data, iters, a, b, depth):
@@ -91,6 +91,34 @@ def test_random_shapes_vs_oracle():
         for depth in ((1, 3, 8) if kernel == "jacobi" else (1,)):
             got = run_device(kernel, data, iters, a, b, depth)
             assert sha(got) == sha(want), (ni, nj, nk, kernel, iters, depth)
+
+
+def test_run_batch_pipelined_host_path():
+    """run_batch (sb_run_host_batch: uploads, sweeps and downloads of
+    consecutive grids overlap) == the oracle per grid; a grid listed again
+    two or more entries later continues from its earlier result; adjacent
+    repeats are rejected before any work."""
+    for kernel, a, b in (("jacobi", 0.0, 1 / 6), ("gs-naive", 0.0, 1 / 6),
+                         ("gs-interleaved", 0.0, 0.15)):
+        gs_ = [make_input({"shape": [22, 14, 10], "pattern": "random", "seed": 50 + i,
+                           "lo": -1.0, "hi": 1.0}) for i in range(3)]
+        want = [oracle.run_serial(kernel, g.data, 5, a, b) for g in gs_]
+        plan = SweepPlan(kernel, "serial", 5, coeffs=StencilCoeffs(a, b))
+        run_batch(plan, gs_)
+        for g, w in zip(gs_, want):
+            assert sha(g.data) == sha(w), kernel
+        # A, B, A, B: the repeats continue from the first pass (10 sweeps each)
+        a0 = make_input({"shape": [22, 14, 10], "pattern": "random", "seed": 60,
+                         "lo": -1.0, "hi": 1.0})
+        b0 = make_input({"shape": [22, 14, 10], "pattern": "random", "seed": 61,
+                         "lo": -1.0, "hi": 1.0})
+        wa = oracle.run_serial(kernel, a0.data, 10, a, b)
+        wb = oracle.run_serial(kernel, b0.data, 10, a, b)
+        run_batch(plan, [a0, b0, a0, b0])
+        assert sha(a0.data) == sha(wa) and sha(b0.data) == sha(wb), kernel
+    g = make_input({"shape": [8, 8, 8], "pattern": "random", "seed": 1, "lo": 0.0, "hi": 1.0})
+    with pytest.raises(ValueError):
+        run_batch(SweepPlan("jacobi", "serial", 1), [g, g])
 
 
 def test_wavefront_plan_depth_and_results(small_cases):

@@ -21,6 +21,7 @@ from paper_1004_1741_b200.sweeps import (
     WavefrontConfig,
     partition_blocks,
     run,
+    run_batch,
     run_pipeline_gs,
     run_threaded_jacobi,
     run_wavefront,
@@ -103,6 +104,25 @@ def test_engine_argument_errors_before_any_work():
         run_wavefront_jacobi(gplan, g)
     with pytest.raises(PlanError):
         run_wavefront_gs(jplan, g)
+
+
+def test_run_batch_validates_before_any_work():
+    """run_batch applies run()'s checks to every grid before touching a
+    device (these raise on a CPU-only host)."""
+    g = create_grid(4, 4, 4, InitPattern.seeded_random(1))
+    h = create_grid(4, 4, 6, InitPattern.seeded_random(2))
+    with pytest.raises(PartitionError):
+        run_batch(SweepPlan("jacobi", "threaded", 1, threads=5), [g])
+    with pytest.raises(PlanError):
+        run_batch(SweepPlan("jacobi", "pipeline", 1), [g])
+    with pytest.raises(PartitionError):
+        run_batch(SweepPlan("jacobi", "wavefront", 2, config=WavefrontConfig(1, 2, 40)), [g])
+    with pytest.raises(ValueError):
+        run_batch(SweepPlan("jacobi", "serial", 1), [g, h])
+    assert run_batch(SweepPlan("jacobi", "serial", 1), []) == []
+    before = g.data.copy()
+    assert run_batch(SweepPlan("jacobi", "serial", 0), [g])[0] is g
+    assert np.array_equal(g.data, before)
 
 
 def test_zero_iterations_return_the_grid_untouched():
