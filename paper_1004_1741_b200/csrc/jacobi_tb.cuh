@@ -245,7 +245,8 @@ __device__ __forceinline__ void produce(const CUtensorMap* src_map, const Jacobi
 // outside a level's trapezoid skip their arithmetic.
 enum StepMode { SLOW = 0, FAST = 1, SEL = 2 };
 
-// One level's update of a thread's RJ rows x 2 cells.  cen: the centre
+// One level's update of a thread's RJ rows x 2 cells in one pass (SEL and
+// SLOW steps).  cen: the centre
 // plane with the south (row 0) and north (row RJ+1) neighbour rows; dn/up:
 // the planes below and above.
 template <class C, int MODE, bool AZ>
@@ -296,9 +297,72 @@ __device__ __forceinline__ void level_update(const double (&cen)[C::RJ + 2][2],
     }
 }
 
-// One plane step of the current item in StepMode MODE.  PH = g mod 3 selects the register rotation statically.  With C::L1S level
-// 1 reads its three input planes straight from the TMA ring (slots g-2,
-// g-1, g); otherwise from register queue Q[0], fed from ring slot g.
+// Phase 1 of a level: the partial sums P = ((((W+E)+S)+N)+D) of the RJ rows
+// x 2 cells.  cen: the centre plane with the south (row 0) and north (row
+// RJ+1) neighbour rows; dn: the plane below.  P may alias dn.
+template <class C>
+__device__ __forceinline__ void level_partial(const double (&cen)[C::RJ + 2][2],
+                                              const double (&dn)[C::RJ][2],
+                                              double (&P)[C::RJ][2]) {
+#pragma unroll
+    for (int r = 0; r < C::RJ; ++r) {
+        const double c0 = cen[r + 1][0], c1 = cen[r + 1][1];
+        const double wv = __shfl_up_sync(0xffffffffu, c1, 1);    // cell i-1 (lane-1)
+        const double ev = __shfl_down_sync(0xffffffffu, c0, 1);  // cell i+2 (lane+1)
+        double acc0 = __dadd_rn(wv, c1), acc1 = __dadd_rn(c0, ev);
+        acc0 = __dadd_rn(acc0, cen[r][0]);
+        acc1 = __dadd_rn(acc1, cen[r][1]);
+        acc0 = __dadd_rn(acc0, cen[r + 2][0]);
+        acc1 = __dadd_rn(acc1, cen[r + 2][1]);
+        P[r][0] = __dadd_rn(acc0, dn[r][0]);
+        P[r][1] = __dadd_rn(acc1, dn[r][1]);
+    }
+}
+
+// Phase 2 of a level: v = a*c + b*(P + U) (the reference association, see
+// jac_final), then the step mode's Dirichlet / trapezoid handling.
+template <class C, int MODE, bool AZ>
+__device__ __forceinline__ void level_finish(const double (&cc)[C::RJ][2],
+                                             const double (&P)[C::RJ][2],
+                                             const double (&up)[C::RJ][2], double (&nv)[C::RJ][2],
+                                             double a, double b, int L, int dj, int k, int gj,
+                                             bool in_i0, bool in_i1, const JacobiParams& p,
+                                             const JState& s) {
+    constexpr int T = C::T, RJ = C::RJ;
+#pragma unroll
+    for (int r = 0; r < RJ; ++r) {
+        const double c0 = cc[r][0], c1 = cc[r][1];
+        const double o0 = jac_final<AZ>(a, b, c0, __dadd_rn(P[r][0], up[r][0]));
+        const double o1 = jac_final<AZ>(a, b, c1, __dadd_rn(P[r][1], up[r][1]));
+        if (MODE == FAST) {
+            nv[r][0] = o0;
+            nv[r][1] = o1;
+        } else if (MODE == SEL) {
+            nv[r][0] = (s.keep0 & (1u << r)) ? c0 : o0;
+            nv[r][1] = (s.keep1 & (1u << r)) ? c1 : o1;
+        } else {
+            const int jr = dj + r, need = T - L;
+            const bool compute = (jr >= -need) && (jr < C::TJ + need) && (k >= 1) &&
+                                 (k <= p.nk) && (gj + r >= 1) && (gj + r <= p.nj);
+            // halo rows/planes keep their value; rows outside the trapezoid: anything
+            nv[r][0] = (compute && in_i0) ? o0 : c0;
+            nv[r][1] = (compute && in_i1) ? o1 : c1;
+        }
+    }
+}
+
+// One plane step of the current item in StepMode MODE.  PH = g mod 3
+// selects the register rotation statically.  With C::L1S level 1 reads its
+// three input planes straight from the TMA ring (slots g-2, g-1, g);
+// otherwise from register queue Q[0], fed from ring slot g.
+//
+// FAST steps run in two phases.  Phase 1 forms every level's partial sum P
+// from data of the previous step only (centre and lower planes in registers, neighbour rows in
+// the exchange buffers / ring) -- T x RJ x 2 independent chains, so the
+// shuffles and adds of all levels overlap.  P overwrites the lower plane,
+// which nothing else needs.  Phase 2 is the short dependent chain through the
+// levels: level L's new plane is level L+1's U.  (SEL/SLOW steps keep the
+// one-pass form: their masks made the two-phase code longer than it gained.)
 template <class C, int MODE, bool AZ, int PH>
 __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CUtensorMap* dst_map,
                                             const JacobiParams& p,
@@ -318,7 +382,6 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
     const int xwb = int(s.g & 1), xrb = int((s.g + 1) & 1);
 
     const int slot = s.g % S;
-    mbar_wait(&full[slot], (s.g / S) & 1);
     const double* cur = ring + size_t(slot) * C::BOXS;
     const double* prv = ring + size_t((s.g + S - 1) % S) * C::BOXS;
     const double* pp = ring + size_t((s.g + S - 2) % S) * C::BOXS;
@@ -327,64 +390,10 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
     const bool in_i0 = (gi >= 1) && (gi <= p.ni);
     const bool in_i1 = (gi + 1 >= 1) && (gi + 1 <= p.ni);
     const double a = p.a, b = p.b;
-    if (!C::L1S) {
-#pragma unroll
-        for (int r = 0; r < RJ; ++r) {
-            const double2 x = lds2(cur + (brow + r) * BW + col);
-            Q[0].q[U][r][0] = x.x;
-            Q[0].q[U][r][1] = x.y;
-        }
-    }
 
-#pragma unroll
-    for (int L = 1; L <= T; ++L) {
+    // emits level L's new plane: exchange rows + queue (L < T) or output
+    auto emit = [&](int L, const double (&nv)[RJ][2]) {
         const int k = pplane - L;
-        double nv[RJ][2];
-        if (C::L1S && L == 1) {
-            double cen[RJ + 2][2], dn[RJ][2], up[RJ][2];
-#pragma unroll
-            for (int r = 0; r < RJ + 2; ++r) {
-                const double2 x = lds2(prv + (brow - 1 + r) * BW + col);
-                cen[r][0] = x.x;
-                cen[r][1] = x.y;
-            }
-#pragma unroll
-            for (int r = 0; r < RJ; ++r) {
-                const double2 x = lds2(pp + (brow + r) * BW + col);
-                const double2 y = lds2(cur + (brow + r) * BW + col);
-                dn[r][0] = x.x;
-                dn[r][1] = x.y;
-                up[r][0] = y.x;
-                up[r][1] = y.y;
-            }
-            level_update<C, MODE, AZ>(cen, dn, up, nv, a, b, L, dj, k, gj, in_i0, in_i1, p, s);
-        } else {
-            LevelQ<C>& In = Q[C::L1S ? L - 2 : L - 1];
-            double2 s2, n2;
-            if (L == 1) {  // neighbour rows of the input plane: from the ring
-                s2 = lds2(prv + (brow - 1) * BW + col);
-                n2 = lds2(prv + (brow + RJ) * BW + col);
-            } else {
-                // south neighbour row: bottom row of warp w-1, north: top row of
-                // warp w+1 (clamped at the tile edge: those rows lie outside the
-                // trapezoid and their values are never used)
-                const double* xr = xb + size_t((L - 2) * C::XB + xrb) * C::XSLOT * C::XROW;
-                s2 = lds2(xr + max(w - 1, 0) * C::XROW + BW + col);
-                n2 = lds2(xr + min(w + 1, NW - 1) * C::XROW + col);
-            }
-            double cen[RJ + 2][2];
-            cen[0][0] = s2.x;
-            cen[0][1] = s2.y;
-            cen[RJ + 1][0] = n2.x;
-            cen[RJ + 1][1] = n2.y;
-#pragma unroll
-            for (int r = 0; r < RJ; ++r) {
-                cen[r + 1][0] = In.q[CC][r][0];
-                cen[r + 1][1] = In.q[CC][r][1];
-            }
-            level_update<C, MODE, AZ>(cen, In.q[D], In.q[U], nv, a, b, L, dj, k, gj, in_i0, in_i1,
-                                      p, s);
-        }
         if (L < T) {
             double* xl = xb + size_t((L - 1) * C::XB + xwb) * C::XSLOT * C::XROW;
             double* xw = xl + w * C::XROW;
@@ -411,6 +420,130 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
                     *reinterpret_cast<double2*>(plane + o) = make_double2(nv[r][0], nv[r][1]);
                 o += uint32_t(p.ni + 2);
             }
+        }
+    };
+    // the centre plane's neighbour rows of level L
+    auto nbr_rows = [&](int L, double (&cen)[RJ + 2][2]) {
+        double2 s2, n2;
+        if (L == 1) {  // from the ring
+            s2 = lds2(prv + (brow - 1) * BW + col);
+            n2 = lds2(prv + (brow + RJ) * BW + col);
+        } else {
+            // south: bottom row of warp w-1, north: top row of warp w+1
+            // (clamped at the tile edge: those rows lie outside the trapezoid
+            // and their values are never used)
+            const double* xr = xb + size_t((L - 2) * C::XB + xrb) * C::XSLOT * C::XROW;
+            s2 = lds2(xr + max(w - 1, 0) * C::XROW + BW + col);
+            n2 = lds2(xr + min(w + 1, NW - 1) * C::XROW + col);
+        }
+        cen[0][0] = s2.x;
+        cen[0][1] = s2.y;
+        cen[RJ + 1][0] = n2.x;
+        cen[RJ + 1][1] = n2.y;
+    };
+
+    if constexpr (MODE == FAST) {
+        // ---- phase 1: partial sums of every level (previous-step data) ----
+        double P1[RJ][2], C1[RJ][2];  // L1S: level 1's P and centre plane (else unused)
+#pragma unroll
+        for (int L = 1; L <= T; ++L) {
+            double cen[RJ + 2][2];
+            nbr_rows(L, cen);
+            if (C::L1S && L == 1) {
+                double dn[RJ][2];
+#pragma unroll
+                for (int r = 0; r < RJ; ++r) {
+                    const double2 x = lds2(prv + (brow + r) * BW + col);
+                    const double2 y = lds2(pp + (brow + r) * BW + col);
+                    cen[r + 1][0] = C1[r][0] = x.x;
+                    cen[r + 1][1] = C1[r][1] = x.y;
+                    dn[r][0] = y.x;
+                    dn[r][1] = y.y;
+                }
+                level_partial<C>(cen, dn, P1);
+            } else {
+                LevelQ<C>& In = Q[C::L1S ? L - 2 : L - 1];
+#pragma unroll
+                for (int r = 0; r < RJ; ++r) {
+                    cen[r + 1][0] = In.q[CC][r][0];
+                    cen[r + 1][1] = In.q[CC][r][1];
+                }
+                level_partial<C>(cen, In.q[D], In.q[D]);
+            }
+        }
+        // ---- phase 2: the level chain ----
+        mbar_wait(&full[slot], (s.g / S) & 1);
+        double U1[RJ][2];
+#pragma unroll
+        for (int r = 0; r < RJ; ++r) {
+            const double2 x = lds2(cur + (brow + r) * BW + col);
+            U1[r][0] = x.x;
+            U1[r][1] = x.y;
+        }
+#pragma unroll
+        for (int L = 1; L <= T; ++L) {
+            double nv[RJ][2];
+            if (C::L1S && L == 1) {
+                level_finish<C, MODE, AZ>(C1, P1, U1, nv, a, b, L, dj, pplane - L, gj, in_i0,
+                                          in_i1, p, s);
+            } else {
+                LevelQ<C>& In = Q[C::L1S ? L - 2 : L - 1];
+                if (L == 1) {
+#pragma unroll
+                    for (int r = 0; r < RJ; ++r) {
+                        In.q[U][r][0] = U1[r][0];
+                        In.q[U][r][1] = U1[r][1];
+                    }
+                }
+                level_finish<C, MODE, AZ>(In.q[CC], In.q[D], In.q[U], nv, a, b, L, dj,
+                                          pplane - L, gj, in_i0, in_i1, p, s);
+            }
+            emit(L, nv);
+        }
+    } else {
+        // SEL / SLOW: one pass per level
+        mbar_wait(&full[slot], (s.g / S) & 1);
+        if (!C::L1S) {
+#pragma unroll
+            for (int r = 0; r < RJ; ++r) {
+                const double2 x = lds2(cur + (brow + r) * BW + col);
+                Q[0].q[U][r][0] = x.x;
+                Q[0].q[U][r][1] = x.y;
+            }
+        }
+#pragma unroll
+        for (int L = 1; L <= T; ++L) {
+            const int k = pplane - L;
+            double nv[RJ][2];
+            double cen[RJ + 2][2];
+            nbr_rows(L, cen);
+            if (C::L1S && L == 1) {
+                double dn[RJ][2], up[RJ][2];
+#pragma unroll
+                for (int r = 0; r < RJ; ++r) {
+                    const double2 x = lds2(prv + (brow + r) * BW + col);
+                    const double2 y = lds2(pp + (brow + r) * BW + col);
+                    const double2 z = lds2(cur + (brow + r) * BW + col);
+                    cen[r + 1][0] = x.x;
+                    cen[r + 1][1] = x.y;
+                    dn[r][0] = y.x;
+                    dn[r][1] = y.y;
+                    up[r][0] = z.x;
+                    up[r][1] = z.y;
+                }
+                level_update<C, MODE, AZ>(cen, dn, up, nv, a, b, L, dj, k, gj, in_i0, in_i1, p,
+                                          s);
+            } else {
+                LevelQ<C>& In = Q[C::L1S ? L - 2 : L - 1];
+#pragma unroll
+                for (int r = 0; r < RJ; ++r) {
+                    cen[r + 1][0] = In.q[CC][r][0];
+                    cen[r + 1][1] = In.q[CC][r][1];
+                }
+                level_update<C, MODE, AZ>(cen, In.q[D], In.q[U], nv, a, b, L, dj, k, gj, in_i0,
+                                          in_i1, p, s);
+            }
+            emit(L, nv);
         }
     }
     const bool out_step = s.n >= 2 * T;
