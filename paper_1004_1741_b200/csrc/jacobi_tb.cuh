@@ -163,7 +163,9 @@ __device__ __forceinline__ double jac_final(double a, double b, double c, double
 }
 
 struct JState {      // per-thread loop state shared by the step functions
-    uint32_t g;      // global plane-step counter (ring phase, exchange parity, rotation)
+    uint32_t g;      // global plane-step counter (exchange parity, rotation)
+    int slot;        // ring slot of step g (= g mod S) and its mbarrier phase parity,
+    uint32_t phase;  // kept incrementally when S is not a power of two
     int n, cq;       // step within the item, consumer queue slot
     ItemInfo it;     // current item
     uint32_t ooff;   // this thread's output cell (row 0) within a plane
@@ -381,10 +383,14 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
     // exchange buffers: written this step / written by the previous step
     const int xwb = int(s.g & 1), xrb = int((s.g + 1) & 1);
 
-    const int slot = s.g % S;
+    // ring slot of this step (power-of-two S: mask and shift of g, else the
+    // incrementally kept slot -- a division by S every step costs issue slots)
+    constexpr bool POW2 = (S & (S - 1)) == 0;
+    const int slot = POW2 ? int(s.g & (S - 1)) : s.slot;
+    const uint32_t phase = POW2 ? (s.g / S) & 1u : s.phase;
     const double* cur = ring + size_t(slot) * C::BOXS;
-    const double* prv = ring + size_t((s.g + S - 1) % S) * C::BOXS;
-    const double* pp = ring + size_t((s.g + S - 2) % S) * C::BOXS;
+    const double* prv = ring + size_t(slot >= 1 ? slot - 1 : slot + S - 1) * C::BOXS;
+    const double* pp = ring + size_t(slot >= 2 ? slot - 2 : slot + S - 2) * C::BOXS;
     const int pplane = it.kb - T + s.n;
     const int gi = it.I0 + di, gj = it.J0 + dj;
     const bool in_i0 = (gi >= 1) && (gi <= p.ni);
@@ -472,7 +478,7 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
             }
         }
         // ---- phase 2: the level chain ----
-        mbar_wait(&full[slot], (s.g / S) & 1);
+        mbar_wait(&full[slot], phase);
         double U1[RJ][2];
 #pragma unroll
         for (int r = 0; r < RJ; ++r) {
@@ -502,7 +508,7 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
         }
     } else {
         // SEL / SLOW: one pass per level
-        mbar_wait(&full[slot], (s.g / S) & 1);
+        mbar_wait(&full[slot], phase);
         if (!C::L1S) {
 #pragma unroll
             for (int r = 0; r < RJ; ++r) {
@@ -564,6 +570,10 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
         produce<C>(src_map, p, ring, full, queue);
     }
     ++s.g;
+    if (!POW2 && ++s.slot == S) {
+        s.slot = 0;
+        s.phase ^= 1u;
+    }
     return ++s.n == it.N;
 }
 
@@ -634,6 +644,8 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
             for (int r = 0; r < C::RJ; ++r) Q[L].q[i][r][0] = Q[L].q[i][r][1] = 0.0;
 
     s.g = 0;
+    s.slot = 0;
+    s.phase = 0;
     s.n = 0;
     s.cq = 0;
     s.it = queue[0];

@@ -362,14 +362,17 @@ static int launch_depth(int T, const double* src, double* dst, int ni, int nj, i
             if (v == 2) SB_L(3, 3, 16, 5, 1, true);
             if (v == 3) SB_L(3, 4, 8, 4, 2, true);
             if (v == 4) SB_L(3, 4, 12, 5, 1, true);
-            if (v == 5) SB_L(3, 4, 8, 5, 1, false, true);
-            SB_L(3, 4, 12, 5, 1, true, true);
+            if (v == 5) SB_L(3, 4, 12, 5, 1, true, true);
+            if (v == 6) SB_L(3, 4, 8, 9, 1, false, true);
+            SB_L(3, 4, 8, 8, 1, false, true);
         case 4:
             if (v == 1) SB_L(4, 2, 16, 4, 1);
             if (v == 2) SB_L(4, 4, 12, 5, 1, true);
             if (v == 3) SB_L(4, 3, 16, 5, 1, true);
             if (v == 4) SB_L(4, 4, 8, 4, 1);
-            SB_L(4, 4, 8, 4, 1, false, true);
+            if (v == 5) SB_L(4, 4, 8, 4, 1, false, true);
+            if (v == 6) SB_L(4, 4, 8, 9, 1, false, true);
+            SB_L(4, 4, 8, 8, 1, false, true);
         case 5: SB_L(5, 2, 12, 3, 1);
         case 6: SB_L(6, 2, 12, 3, 1);
         case 7: SB_L(7, 2, 12, 3, 1);
