@@ -356,7 +356,8 @@ static int launch_depth(int T, const double* src, double* dst, int ni, int nj, i
         case 2:
             if (v == 1) SB_L(2, 4, 8, 4, 2);
             if (v == 2) SB_L(2, 4, 12, 5, 1, true);
-            SB_L(2, 4, 8, 4, 2, true);
+            if (v == 5) SB_L(2, 4, 8, 4, 2, true);
+            SB_L(2, 4, 8, 8, 1, false, true);
         case 3:
             if (v == 1) SB_L(3, 2, 16, 4, 1);
             if (v == 2) SB_L(3, 3, 16, 5, 1, true);
