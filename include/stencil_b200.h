@@ -22,6 +22,9 @@
  *                                    <- run_threaded_jacobi's k-slab split
  *                                       (sweeps/threaded.py:28-59, :39)
  *                                       across GPUs (z-slabs + halo exchange)
+ *   sb_gs_slabs / sb_gs_slab_layout  <- run_pipeline_gs's pipelined order
+ *                                       (sweeps/threaded.py:62-96) as a
+ *                                       cross-GPU z-pipeline of slabs
  *
  * Grid layout (reference grid.py:61-91): (nk+2) x (nj+2) x (ni+2) doubles,
  * C order, i unit stride; interior cell (k,j,i) at padded (k+1,j+1,i+1);
@@ -215,6 +218,28 @@ int sb_jacobi_slabs(int nslabs, const int* devices, double* const* slabs,
                     double* const* scratch, int64_t ni, int64_t nj, int64_t nk,
                     int64_t iters, double a, double b, int depth, void* const* streams,
                     int* result_in_scratch);
+
+/*
+ * Gauss-Seidel slab layout: slab `slab` of nslabs owns the global padded
+ * planes [*own_lo, *own_hi) (partition_blocks(nk, nslabs)); its local grid
+ * holds global planes own_lo-1 .. own_hi, i.e. (own_hi-own_lo) interior
+ * planes between two ghost planes.  SB_ERR_PARTITION when nslabs > nk.
+ */
+int sb_gs_slab_layout(int64_t nk, int nslabs, int slab, int64_t* own_lo, int64_t* own_hi);
+
+/*
+ * Multi-slab Gauss-Seidel in one process (the cross-GPU z-pipeline):
+ * slabs[g] is a device grid on devices[g] laid out per sb_gs_slab_layout and
+ * filled with the initial global planes own_lo-1 .. own_hi; streams[g] a
+ * stream on devices[g] (slabs sharing a device must share its stream).
+ * Runs `iters` in-place sweeps of `kernel` (SB_KERNEL_GS_*): sweep s of slab
+ * g starts once slab g-1 finished sweep s and slab g+1 sweep s-1 (ghost
+ * planes copied between them), so slabs on different GPUs run as a
+ * pipeline.  Owned planes end bitwise equal to sb_gs on the whole grid.
+ * Synchronous.
+ */
+int sb_gs_slabs(int nslabs, const int* devices, double* const* slabs, int64_t ni, int64_t nj,
+                int64_t nk, int64_t iters, double b, int kernel, void* const* streams);
 
 #ifdef __cplusplus
 }

@@ -384,4 +384,112 @@ int sb_jacobi_slabs(int nslabs, const int* devices, double* const* slabs, double
     return SB_OK;
 }
 
+// Gauss-Seidel across slabs: the cross-GPU z-pipeline form of the reference's
+// pipeline GS (sweeps/threaded.py:62-96).  Slab g owns the
+// interior planes partition_blocks(nk, nslabs)[g]; its local grid holds them
+// between two ghost planes that act as its k-halo: below, slab g-1's last
+// plane after the current sweep (new values: the D neighbour of the
+// lexicographic order); above, slab g+1's first plane after the previous
+// sweep (old values: U).  One in-place GS sweep of the local grid is then
+// exactly the global sweep on the owned planes, so results are bitwise
+// identical to one grid.  Sweep s of slab g waits for sweep s of slab g-1
+// and sweep s-1 of slab g+1: the slabs advance as a pipeline, S/(S+G-1)
+// efficient for S sweeps on G slabs.
+int sb_gs_slab_layout(int64_t nk, int nslabs, int slab, int64_t* own_lo, int64_t* own_hi) {
+    clear_error();
+    if (nslabs < 1 || nslabs > nk)
+        return fail(SB_ERR_PARTITION, "cannot split nk=%lld planes into %d slabs", (long long)nk, nslabs);
+    if (slab < 0 || slab >= nslabs) return fail(SB_ERR_ARGUMENT, "slab %d of %d", slab, nslabs);
+    if (!own_lo || !own_hi) return fail(SB_ERR_ARGUMENT, "null pointer");
+    int64_t lo, hi;
+    part(nk, nslabs, slab, &lo, &hi);
+    *own_lo = lo + 1;  // padded global plane indices
+    *own_hi = hi + 1;
+    return SB_OK;
+}
+
+int sb_gs_slabs(int nslabs, const int* devices, double* const* slabs, int64_t ni, int64_t nj,
+                int64_t nk, int64_t iters, double b, int kernel, void* const* streams) {
+    clear_error();
+    int rc = check_dims(ni, nj, nk);
+    if (rc) return rc;
+    if (iters < 0) return fail(SB_ERR_PLAN, "iter_end must be >= 0, got %lld", (long long)iters);
+    if (kernel != SB_KERNEL_GS_NAIVE && kernel != SB_KERNEL_GS_INTERLEAVED)
+        return fail(SB_ERR_PLAN, "sb_gs_slabs runs the Gauss-Seidel kernels, got %d", kernel);
+    if (!devices || !slabs || !streams) return fail(SB_ERR_ARGUMENT, "null pointer");
+    struct Slab {
+        int dev;
+        double* g;
+        cudaStream_t st;
+        int64_t nkl;                   // owned planes (local interior)
+        cudaEvent_t done, got_lo, got_hi;  // sweep finished / ghost copies finished
+    };
+    std::vector<Slab> S(nslabs);
+    for (int g = 0; g < nslabs; ++g) {
+        int64_t lo, hi;
+        if ((rc = sb_gs_slab_layout(nk, nslabs, g, &lo, &hi))) return rc;
+        if (!slabs[g]) return fail(SB_ERR_ARGUMENT, "null slab %d", g);
+        S[g].dev = devices[g];
+        S[g].g = slabs[g];
+        S[g].st = static_cast<cudaStream_t>(streams[g]);
+        S[g].nkl = hi - lo;
+    }
+    if (iters == 0) return SB_OK;
+    const int64_t plane = (ni + 2) * (nj + 2);
+    const size_t pbytes = size_t(plane) * sizeof(double);
+    cudaError_t e;
+    for (int g = 0; g < nslabs; ++g) {
+        if ((e = cudaSetDevice(S[g].dev)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+        for (int h : {g - 1, g + 1})
+            if (h >= 0 && h < nslabs && S[h].dev != S[g].dev) {
+                int can = 0;
+                cudaDeviceCanAccessPeer(&can, S[g].dev, S[h].dev);
+                if (can) {
+                    e = cudaDeviceEnablePeerAccess(S[h].dev, 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                    else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+                }
+            }
+        for (cudaEvent_t* ev : {&S[g].done, &S[g].got_lo, &S[g].got_hi})
+            if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(e, "cudaEventCreate");
+    }
+    for (int64_t sw = 0; sw < iters; ++sw) {
+        for (int g = 0; g < nslabs; ++g) {
+            Slab& X = S[g];
+            cudaSetDevice(X.dev);
+            if (g > 0) {  // ghost below: slab g-1's last plane after this sweep
+                Slab& Y = S[g - 1];
+                cudaStreamWaitEvent(X.st, Y.done, 0);
+                if ((e = cudaMemcpyPeerAsync(X.g, X.dev, Y.g + Y.nkl * plane, Y.dev, pbytes, X.st)) !=
+                    cudaSuccess)
+                    return cuda_fail(e, "ghost copy (below)");
+                cudaEventRecord(X.got_lo, X.st);
+                // slab g-1 read this slab's first plane (old) before it changes
+                if (sw > 0) cudaStreamWaitEvent(X.st, Y.got_hi, 0);
+            }
+            if (g + 1 < nslabs && sw > 0) {  // ghost above: slab g+1's first plane, previous sweep
+                Slab& Y = S[g + 1];
+                cudaStreamWaitEvent(X.st, Y.done, 0);
+                if ((e = cudaMemcpyPeerAsync(X.g + (X.nkl + 1) * plane, X.dev, Y.g + plane, Y.dev, pbytes,
+                                             X.st)) != cudaSuccess)
+                    return cuda_fail(e, "ghost copy (above)");
+                cudaEventRecord(X.got_hi, X.st);
+                // slab g+1 copied this slab's last plane (previous sweep) before it changes
+                cudaStreamWaitEvent(X.st, Y.got_lo, 0);
+            }
+            if ((rc = sb_gs(X.g, ni, nj, X.nkl, 1, b, kernel, X.st))) return rc;
+            cudaEventRecord(X.done, X.st);
+        }
+    }
+    rc = SB_OK;
+    for (int g = 0; g < nslabs; ++g) {
+        cudaSetDevice(S[g].dev);
+        if ((e = cudaStreamSynchronize(S[g].st)) != cudaSuccess && rc == SB_OK)
+            rc = cuda_fail(e, "slab sweeps");
+        for (cudaEvent_t ev : {S[g].done, S[g].got_lo, S[g].got_hi}) cudaEventDestroy(ev);
+    }
+    return rc;
+}
+
 }  // extern "C"

@@ -142,3 +142,95 @@ class SlabEngine:
             self.period(t)
             left -= t
         self.wait()
+
+
+# ---------------------------------------------------------------------------
+# Gauss-Seidel: the cross-GPU z-pipeline (reference pipeline GS,
+# sweeps/threaded.py:62-96 / PAPER:336-345, with slabs of planes as stages).
+
+
+def gs_slab_layout(nk, nslabs, slab):
+    """(own_lo, own_hi) global padded planes of a GS slab; its local grid
+    holds global planes own_lo-1 .. own_hi (one ghost plane each side).
+    Mirrors sb_gs_slab_layout (host.cu)."""
+    lo, hi = partition_blocks(nk, nslabs)[slab]
+    return lo + 1, hi + 1
+
+
+def gpu_gs_compute(ni, nj, b, kernel):
+    """compute(grid, nk_local, sweeps): in-place GS sweeps of a local grid on
+    the current stream (sb_gs; the ghost planes are its k-halo)."""
+    import torch
+
+    lib = _lib.load()
+    kid = _lib.KERNEL_IDS[kernel]
+
+    def compute(grid, nkl, sweeps):
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(lib.sb_gs(grid.data_ptr(), ni, nj, nkl, sweeps, b, kid, stream))
+
+    return compute
+
+
+class GsSlabEngine:
+    """This rank's slab of a pipelined multi-GPU Gauss-Seidel run.
+
+    Sweep s of rank g needs rank g-1's last plane after sweep s (the new
+    D values of the lexicographic order) and rank g+1's first plane after
+    sweep s-1 (the old U values); with those as the ghost planes, one
+    in-place sweep of the local grid equals the global sweep on the owned
+    planes, bitwise.  Ranks therefore advance as a pipeline, one plane sent
+    each way per sweep and interface (S/(S+G-1) efficient for S sweeps)."""
+
+    def __init__(self, ni, nj, nk, rank, world, compute, like, group=None):
+        import torch
+
+        self.ni, self.nj, self.nk = ni, nj, nk
+        self.rank, self.world, self.group = rank, world, group
+        self.compute = compute
+        self.own_lo, self.own_hi = gs_slab_layout(nk, world, rank)
+        self.nkl = self.own_hi - self.own_lo
+        self.grid = torch.empty((self.nkl + 2, nj + 2, ni + 2), dtype=like.dtype, device=like.device)
+        self.sends = []
+
+    def load_global(self, global_data):
+        """Fill the local grid (owned + ghost planes) from the global grid."""
+        import torch
+
+        part = global_data[self.own_lo - 1:self.own_hi + 1]
+        if not torch.is_tensor(part):
+            part = torch.from_numpy(part)
+        self.grid.copy_(part)
+
+    def owned(self):
+        return self.grid[1:self.nkl + 1]
+
+    def sweep(self, s, last=False):
+        """Sweep number s (0-based) of this slab; `last`: no sweep follows, so
+        the first plane is not sent down (nothing would receive it)."""
+        import torch.distributed as dist
+
+        recvs = []
+        if self.rank > 0:  # new values of the plane below
+            recvs.append(dist.irecv(self.grid[0], self.rank - 1, self.group))
+        if self.rank + 1 < self.world and s > 0:  # old values of the plane above
+            recvs.append(dist.irecv(self.grid[self.nkl + 1], self.rank + 1, self.group))
+        for w in self.sends + recvs:  # sent planes are overwritten by this sweep
+            w.wait()
+        self.compute(self.grid, self.nkl, 1)
+        self.sends = []
+        if self.rank + 1 < self.world:
+            self.sends.append(dist.isend(self.grid[self.nkl], self.rank + 1, self.group))
+        if self.rank > 0 and not last:
+            self.sends.append(dist.isend(self.grid[1], self.rank - 1, self.group))
+
+    def run(self, iters):
+        if self.world == 1:
+            if iters:
+                self.compute(self.grid, self.nkl, iters)
+            return
+        for s in range(iters):
+            self.sweep(s, last=(s == iters - 1))
+        for w in self.sends:
+            w.wait()
+        self.sends = []

@@ -135,3 +135,131 @@ def test_slab_engine_single_rank_matches_oracle():
     torch.cuda.synchronize()
     want = oracle.run_serial("jacobi", g.data, 10, 0.0, 1 / 6)
     assert sha(eng.owned().cpu().numpy()) == sha(want[1:-1])
+
+
+# ---------------------------------------------------------------------------
+# Gauss-Seidel cross-slab pipeline
+
+
+def cpu_gs_compute(kernel, b):
+    """Oracle stand-in for sb_gs on a local slab grid (test infrastructure)."""
+    import torch
+
+    def compute(grid, nkl, sweeps):
+        out = oracle.run_serial(kernel, grid.numpy(), sweeps, 0.0, b)
+        grid.copy_(torch.from_numpy(out))
+
+    return compute
+
+
+def _gloo_gs_worker(rank, world, port, spec, iters, kernel, b, result_path):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1004_1741_b200.slabs import GsSlabEngine, gs_slab_layout
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = make_input(spec)
+    eng = GsSlabEngine(g.ni, g.nj, g.nk, rank, world, cpu_gs_compute(kernel, b),
+                       like=torch.empty(0, dtype=torch.float64))
+    eng.load_global(g.data)
+    eng.run(iters)
+    owned = eng.owned().contiguous()
+    if rank == 0:
+        parts = [owned]
+        for r in range(1, world):
+            lo, hi = gs_slab_layout(g.nk, world, r)
+            t = torch.empty((hi - lo, g.nj + 2, g.ni + 2), dtype=torch.float64)
+            dist.recv(t, src=r)
+            parts.append(t)
+        np.save(result_path, torch.cat(parts).numpy())
+    else:
+        dist.send(owned, dst=0)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,shape,iters,kernel", [
+    (2, (12, 10, 9), 6, "gs-naive"),
+    (3, (9, 8, 7), 5, "gs-interleaved"),
+    (3, (6, 5, 3), 4, "gs-naive"),
+])
+def test_gloo_gs_pipeline_bitwise_equal_single_grid(tmp_path, world, shape, iters, kernel):
+    """The GS z-pipeline (real exchange code, oracle compute) on world ranks
+    equals the serial reference sweep bit for bit."""
+    import torch.multiprocessing as mp
+
+    spec = {"shape": list(shape), "pattern": "random", "seed": 8, "lo": -1.0, "hi": 1.0}
+    out = tmp_path / "owned.npy"
+    mp.start_processes(_gloo_gs_worker, args=(world, _free_port(), spec, iters, kernel, 1 / 6,
+                                              str(out)),
+                       nprocs=world, join=True, start_method="spawn")
+    got = np.load(out)
+    want = oracle.run_serial(kernel, make_input(spec).data, iters, 0.0, 1 / 6)[1:-1]
+    assert sha(got) == sha(want)
+
+
+def test_gs_slab_layout_matches_c_abi():
+    import ctypes
+
+    from paper_1004_1741_b200 import _lib
+    from paper_1004_1741_b200.errors import PartitionError
+    from paper_1004_1741_b200.slabs import gs_slab_layout
+
+    lib = _lib.load()
+    for nk, n in ((10, 3), (7, 7), (64, 5), (2048, 8)):
+        for s in range(n):
+            lo, hi = ctypes.c_int64(), ctypes.c_int64()
+            _lib.check(lib.sb_gs_slab_layout(nk, n, s, ctypes.byref(lo), ctypes.byref(hi)))
+            assert (lo.value, hi.value) == gs_slab_layout(nk, n, s)
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    with pytest.raises(PartitionError):
+        _lib.check(lib.sb_gs_slab_layout(3, 4, 0, ctypes.byref(lo), ctypes.byref(hi)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nslabs,iters,kernel", [(2, 5, "gs-naive"), (3, 7, "gs-interleaved"),
+                                                 (5, 3, "gs-naive")])
+def test_c_abi_gs_slabs_on_one_gpu(nslabs, iters, kernel):
+    """sb_gs_slabs with every slab on GPU 0 (one stream) == the serial sweep."""
+    import ctypes
+
+    import torch
+
+    from paper_1004_1741_b200 import _lib
+    from paper_1004_1741_b200.slabs import gs_slab_layout
+
+    lib = _lib.load()
+    spec = {"shape": [40, 36, 50], "pattern": "random", "seed": 11, "lo": -1.0, "hi": 1.0}
+    g = make_input(spec)
+    want = oracle.run_serial(kernel, g.data, iters, 0.0, 1 / 6)
+    bufs = []
+    for s in range(nslabs):
+        lo, hi = gs_slab_layout(g.nk, nslabs, s)
+        bufs.append(torch.from_numpy(np.ascontiguousarray(g.data[lo - 1:hi + 1])).cuda())
+    st = torch.cuda.Stream()
+    devs = (ctypes.c_int * nslabs)(*([0] * nslabs))
+    pa = (ctypes.c_void_p * nslabs)(*[t.data_ptr() for t in bufs])
+    ps = (ctypes.c_void_p * nslabs)(*([st.cuda_stream] * nslabs))
+    _lib.check(lib.sb_gs_slabs(nslabs, devs, pa, g.ni, g.nj, g.nk, iters, 1 / 6,
+                               _lib.KERNEL_IDS[kernel], ps))
+    owned = [t[1:-1].cpu().numpy() for t in bufs]
+    assert sha(np.concatenate(owned)) == sha(want[1:-1])
+
+
+@pytest.mark.gpu
+def test_gs_slab_engine_single_rank_matches_oracle():
+    import torch
+
+    from paper_1004_1741_b200.slabs import GsSlabEngine, gpu_gs_compute
+
+    spec = {"shape": [62, 20, 33], "pattern": "random", "seed": 4, "lo": -1.0, "hi": 1.0}
+    g = make_input(spec)
+    eng = GsSlabEngine(g.ni, g.nj, g.nk, 0, 1, gpu_gs_compute(g.ni, g.nj, 1 / 6, "gs-naive"),
+                       like=torch.empty(0, dtype=torch.float64, device="cuda"))
+    eng.load_global(g.data)
+    eng.run(6)
+    torch.cuda.synchronize()
+    want = oracle.run_serial("gs-naive", g.data, 6, 0.0, 1 / 6)
+    assert sha(eng.owned().cpu().numpy()) == sha(want[1:-1])
