@@ -57,7 +57,9 @@ struct JacobiParams {
     int tiles_i, tiles_j;    // output tiles per plane
     int kblk;                // planes per work item
     int kblocks;             // ceil((klast - kfirst) / kblk)
-    int items;               // tiles_i * tiles_j * kblocks
+    int items;               // tiles_i * tiles_j * kblocks, or the length of `list`
+    const int4* list;        // null: regular k-block-major items; else explicit items
+                             // (tile, first plane, end plane, -) claimed in list order
     double a, b;
     int* counter;            // work counter (zeroed before launch)
     double* dst;             // output grid
@@ -128,14 +130,22 @@ __device__ __forceinline__ ItemInfo decode_item(const JacobiParams& p, int item)
         it.I0 = it.J0 = it.kb = it.N = 0;
         return it;
     }
-    const int per_block = p.tiles_i * p.tiles_j;
-    const int kbi = item / per_block;
-    const int t = item - kbi * per_block;
+    int t, ke;
+    if (p.list) {
+        const int4 v = __ldg(p.list + item);
+        t = v.x;
+        it.kb = v.y;
+        ke = v.z;
+    } else {
+        const int per_block = p.tiles_i * p.tiles_j;
+        const int kbi = item / per_block;
+        t = item - kbi * per_block;
+        it.kb = p.kfirst + kbi * p.kblk;
+        ke = min(it.kb + p.kblk, p.klast);
+    }
     const int ti = t % p.tiles_i, tj = t / p.tiles_i;
     it.I0 = C::TO * ti;
     it.J0 = 1 + C::TJ * tj;
-    it.kb = p.kfirst + kbi * p.kblk;
-    const int ke = min(it.kb + p.kblk, p.klast);
     it.N = ke - it.kb + 2 * C::T;
     return it;
 }

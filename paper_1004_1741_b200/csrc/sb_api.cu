@@ -206,65 +206,19 @@ __global__ void triad_kernel(double* __restrict__ a, const double* __restrict__ 
 // ---------------------------------------------------------------------------
 // temporally blocked launch
 
-// Work-item length along k (planes per (tile, k-block) item).
-//  * T = 1, 2 (HBM-bound): short blocks.  Work items are handed out
-//    k-block-major, so short blocks keep every resident CTA within a few
-//    planes of each other and the overlapping halo rows/columns that
-//    neighbouring tiles re-read hit L2 (measured on B200, 1024^3: T=1 327 ->
-//    382 GLUP/s at 8 planes; T=2 605 -> 618 at 64).
-//  * T >= 3 (compute-bound): every item pays 2T warm-up steps plus a fixed
-//    cost (fitted: ~4 steps), and the last wave of items leaves CTAs idle.
-//    Among the block lengths ceil(nk / nb) and the "about 8 items per CTA"
-//    length, take the one minimising the makespan of the dynamic schedule
-//    (items claimed in order by the first free CTA), simulated once per shape.
-static int64_t schedule_span(int T, int tiles, int nkout, int grid, int kb) {
-    std::priority_queue<int64_t, std::vector<int64_t>, std::greater<int64_t>> q;
-    for (int c = 0; c < grid; ++c) q.push(0);
-    int64_t span = 0;
-    for (int blk = 0; (int64_t)blk * kb < nkout; ++blk) {
-        const int64_t cost = std::min(kb, nkout - blk * kb) + 2 * T + 4;
-        for (int t = 0; t < tiles; ++t) {
-            const int64_t f = q.top() + cost;
-            q.pop();
-            q.push(f);
-            span = std::max(span, f);
+// Per tile: 1 if the tile's computed region touches the i/j boundary (its
+// interior steps run in SEL mode; jacobi_tb.cuh, the kernel's ij_in).
+template <class C>
+static std::vector<char> border_tiles(int ni, int nj, int tiles_i, int tiles_j) {
+    std::vector<char> v(size_t(tiles_i) * tiles_j);
+    for (int tj = 0; tj < tiles_j; ++tj)
+        for (int ti = 0; ti < tiles_i; ++ti) {
+            const int I0 = C::TO * ti, jlo = 1 + C::TJ * tj - (C::T - 1);
+            const bool in = (I0 - C::H >= 1) && (I0 - C::H + C::BW - 1 <= ni) && (jlo >= 1) &&
+                            (jlo + C::ROWS - 1 <= nj);
+            v[size_t(tj) * tiles_i + ti] = in ? 0 : 1;
         }
-    }
-    return span;
-}
-
-static int pick_kblock(int T, int tiles, int nkout, int grid) {
-    if (T == 1) return 8;
-    if (T == 2) return 64;
-    static std::mutex mu;
-    static std::map<std::tuple<int, int, int, int>, int> cache;
-    const auto key = std::make_tuple(T, tiles, nkout, grid);
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = cache.find(key);
-        if (it != cache.end()) return it->second;
-    }
-    const int64_t want = (int64_t)grid * 8;
-    int kb0 = (int)std::min<int64_t>(((int64_t)tiles * nkout + want - 1) / want, nkout);
-    kb0 = std::max(kb0, std::min(8 * T, nkout));
-    std::vector<int> cands{kb0};
-    for (int nb = 1; nb <= 64; ++nb) {
-        const int kb = (nkout + nb - 1) / nb;
-        if (kb < 4 * T && nb > 1) break;
-        cands.push_back(kb);
-    }
-    int best_kb = kb0;
-    int64_t best = INT64_MAX;
-    for (int kb : cands) {
-        const int64_t sp = schedule_span(T, tiles, nkout, grid, kb);
-        if (sp < best || (sp == best && kb > best_kb)) {
-            best = sp;
-            best_kb = kb;
-        }
-    }
-    std::lock_guard<std::mutex> lk(mu);
-    cache[key] = best_kb;
-    return best_kb;
+    return v;
 }
 
 template <class C, bool AZ>
@@ -314,6 +268,18 @@ static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk
     p.kblk = kb;
     p.kblocks = (nkout + kb - 1) / kb;
     p.items = tiles * p.kblocks;
+    p.list = nullptr;
+    if (kb_env <= 0) {
+        const int4* list;
+        int count;
+        if ((rc = item_list(C::T, p.tiles_i, p.tiles_j, border_tiles<C>(ni, nj, p.tiles_i, p.tiles_j),
+                            kfirst, klast, grid, kb, &list, &count)))
+            return rc;
+        if (list) {
+            p.list = list;
+            p.items = count;
+        }
+    }
     p.a = a;
     p.b = b;
     p.counter = counters;

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <vector>
 
 namespace sb {
 
@@ -20,5 +21,11 @@ int jacobi_generic_sweep(const double* src, double* dst, int ni, int nj, int nk,
                          cudaStream_t st);
 int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,
            cudaStream_t st);
+
+// work schedules of the temporally blocked Jacobi launch (sched.cu)
+int64_t schedule_span(int T, int tiles, int nkout, int grid, int kb);
+int pick_kblock(int T, int tiles, int nkout, int grid);
+int item_list(int T, int tiles_i, int tiles_j, const std::vector<char>& border, int kfirst,
+              int klast, int grid, int kb, const int4** out, int* count);
 
 }  // namespace sb
