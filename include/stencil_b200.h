@@ -86,6 +86,22 @@ int sb_device_count(void);
 int sb_max_depth(void);
 
 /*
+ * Diagnostic (host only, no GPU work): the work items of one fused launch
+ * of `sweeps` (1..sb_max_depth()) Jacobi sweeps writing planes
+ * [k_out_lo, k_out_hi) of an ni x nj grid (even ni: the tiled kernel) on a
+ * device with `ctas` resident CTAs, in the order the CTAs claim them.  Item
+ * x is items[4x..4x+3] = (tile_i, tile_j, k0, k1): output columns
+ * [TO*tile_i, TO*tile_i + TO), rows [1 + TJ*tile_j, 1 + TJ*tile_j + TJ),
+ * planes [k0, k1).  Writes min(cap, *count) items; dims (may be NULL)
+ * receives (TO, TJ, tiles_i, tiles_j).  Every (tile, plane) of the launch
+ * appears in exactly one item -- tests/test_lib.py checks that property.
+ * No Python-reference counterpart: it exposes the schedule of
+ * sb_jacobi / sb_jacobi_planes ("Schedule").
+ */
+int sb_jacobi_schedule(int sweeps, int64_t ni, int64_t nj, int64_t k_out_lo, int64_t k_out_hi,
+                       int ctas, int32_t* items, int64_t cap, int64_t* count, int32_t* dims);
+
+/*
  * Jacobi sweeps on device memory.  `grid` and `scratch` are device
  * pointers to two distinct padded grids; `scratch` needs no initialisation
  * (its halo is copied from `grid` on the stream).  Advances `iters` sweeps,

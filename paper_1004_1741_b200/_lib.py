@@ -37,6 +37,9 @@ SIGNATURES = {
     "sb_last_error": (ctypes.c_char_p, []),
     "sb_device_count": (_int, []),
     "sb_max_depth": (_int, []),
+    "sb_jacobi_schedule": (_int, [_int, _i64, _i64, _i64, _i64, _int,
+                                  ctypes.POINTER(ctypes.c_int32), _i64, ctypes.POINTER(_i64),
+                                  ctypes.POINTER(ctypes.c_int32)]),
     "sb_jacobi": (_int, [_vp, _vp, _i64, _i64, _i64, _i64, _dbl, _dbl, _int, _vp,
                          ctypes.POINTER(_int)]),
     "sb_gs": (_int, [_vp, _i64, _i64, _i64, _i64, _dbl, _int, _vp]),
@@ -118,6 +121,23 @@ def require_device():
 
 def max_depth():
     return load().sb_max_depth()
+
+
+def jacobi_schedule(sweeps, ni, nj, k_lo, k_hi, ctas):
+    """Work items of one fused Jacobi launch (sb_jacobi_schedule; host only):
+    returns (items, (TO, TJ, tiles_i, tiles_j)) with items an (n, 4) int32
+    array of (tile_i, tile_j, k0, k1) in claim order."""
+    import numpy as np
+
+    lib = load()
+    n = _i64(0)
+    dims = (ctypes.c_int32 * 4)()
+    check(lib.sb_jacobi_schedule(sweeps, ni, nj, k_lo, k_hi, ctas, None, 0, ctypes.byref(n), dims))
+    items = np.zeros((max(1, n.value), 4), dtype=np.int32)
+    check(lib.sb_jacobi_schedule(sweeps, ni, nj, k_lo, k_hi, ctas,
+                                 items.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), n.value,
+                                 ctypes.byref(n), dims))
+    return items[:n.value], tuple(dims)
 
 
 def pinned_array(shape):

@@ -221,6 +221,27 @@ static std::vector<char> border_tiles(int ni, int nj, int tiles_i, int tiles_j) 
     return v;
 }
 
+// Tile grid and k-block length of one launch (shared by the launch and the
+// schedule query sb_jacobi_schedule, so both see the same decomposition).
+struct TbPlan {
+    int tiles_i, tiles_j, kb;
+    bool list_ok;  // explicit item list allowed (not overridden by SB_KBLK)
+};
+
+template <class C>
+static TbPlan tb_plan(int ni, int nj, int kfirst, int klast, int grid) {
+    TbPlan pl;
+    pl.tiles_i = (ni + 1 + C::TO - 1) / C::TO;  // tiles [TO*t, TO*t+TO) must cover [1, ni]
+    pl.tiles_j = (nj + C::TJ - 1) / C::TJ;
+    const int nkout = klast - kfirst;
+    int kb = pick_kblock(C::T, pl.tiles_i * pl.tiles_j, nkout, grid);
+    static const int kb_env = getenv("SB_KBLK") ? atoi(getenv("SB_KBLK")) : 0;  // tuning
+    if (kb_env > 0) kb = kb_env;
+    pl.kb = std::max(1, std::min(kb, nkout));
+    pl.list_ok = kb_env <= 0;
+    return pl;
+}
+
 template <class C, bool AZ>
 static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk, int kfirst,
                           int klast, double a, double b, cudaStream_t st) {
@@ -254,22 +275,20 @@ static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk
     p.ni = ni;
     p.nj = nj;
     p.nk = nk;
-    p.tiles_i = (ni + 1 + C::TO - 1) / C::TO;  // tiles [TO*t, TO*t+TO) must cover [1, ni]
-    p.tiles_j = (nj + C::TJ - 1) / C::TJ;
     const int grid = occ;  // resident CTAs
+    const TbPlan pl = tb_plan<C>(ni, nj, kfirst, klast, grid);
+    p.tiles_i = pl.tiles_i;
+    p.tiles_j = pl.tiles_j;
     const int tiles = p.tiles_i * p.tiles_j;
     const int nkout = klast - kfirst;
-    int kb = pick_kblock(C::T, tiles, nkout, grid);
-    static const int kb_env = getenv("SB_KBLK") ? atoi(getenv("SB_KBLK")) : 0;  // tuning
-    if (kb_env > 0) kb = kb_env;
-    kb = min(kb, nkout);
+    const int kb = pl.kb;
     p.kfirst = kfirst;
     p.klast = klast;
     p.kblk = kb;
     p.kblocks = (nkout + kb - 1) / kb;
     p.items = tiles * p.kblocks;
     p.list = nullptr;
-    if (kb_env <= 0) {
+    if (pl.list_ok) {
         const int4* list;
         int count;
         if ((rc = item_list(C::T, p.tiles_i, p.tiles_j, border_tiles<C>(ni, nj, p.tiles_i, p.tiles_j),
@@ -309,11 +328,11 @@ static int jcfg_variant() {
     return v;
 }
 
-static int launch_depth(int T, const double* src, double* dst, int ni, int nj, int nk, int kfirst,
-                        int klast, double a, double b, cudaStream_t st) {
-    if (klast <= kfirst) return SB_OK;
+// Calls f(JacobiCfg<...>{}) with the tile configuration of depth T.
+template <class F>
+static int with_cfg(int T, F&& f) {
     const int v = jcfg_variant();
-#define SB_L(...) return launch_tb<JacobiCfg<__VA_ARGS__>>(src, dst, ni, nj, nk, kfirst, klast, a, b, st)
+#define SB_L(...) return f(JacobiCfg<__VA_ARGS__>{})
     switch (T) {
         case 1:
             if (v == 1) SB_L(1, 2, 8, 4, 4);
@@ -347,6 +366,44 @@ static int launch_depth(int T, const double* src, double* dst, int ni, int nj, i
     }
 #undef SB_L
     return fail(SB_ERR_PLAN, "unsupported depth %d", T);
+}
+
+static int launch_depth(int T, const double* src, double* dst, int ni, int nj, int nk, int kfirst,
+                        int klast, double a, double b, cudaStream_t st) {
+    if (klast <= kfirst) return SB_OK;
+    return with_cfg(T, [&](auto cfg) {
+        return launch_tb<decltype(cfg)>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+    });
+}
+
+// The work items of one launch (see sb_jacobi_schedule).
+template <class C>
+static int schedule_query(int ni, int nj, int kfirst, int klast, int ctas, int32_t* items,
+                          int64_t cap, int64_t* count, int32_t* dims) {
+    const TbPlan pl = tb_plan<C>(ni, nj, kfirst, klast, ctas);
+    std::vector<int4> v;
+    if (pl.list_ok)
+        v = build_item_list(C::T, pl.tiles_i, pl.tiles_j,
+                            border_tiles<C>(ni, nj, pl.tiles_i, pl.tiles_j), kfirst, klast, ctas,
+                            pl.kb);
+    if (v.empty())  // the regular decomposition, in claim order (k-block major)
+        for (int k0 = kfirst; k0 < klast; k0 += pl.kb)
+            for (int t = 0; t < pl.tiles_i * pl.tiles_j; ++t)
+                v.push_back(make_int4(t, k0, std::min(k0 + pl.kb, klast), 0));
+    if (dims) {
+        dims[0] = C::TO;
+        dims[1] = C::TJ;
+        dims[2] = pl.tiles_i;
+        dims[3] = pl.tiles_j;
+    }
+    *count = (int64_t)v.size();
+    for (int64_t x = 0; x < std::min<int64_t>(cap, (int64_t)v.size()); ++x) {
+        items[4 * x + 0] = v[x].x % pl.tiles_i;
+        items[4 * x + 1] = v[x].x / pl.tiles_i;
+        items[4 * x + 2] = v[x].y;
+        items[4 * x + 3] = v[x].z;
+    }
+    return SB_OK;
 }
 
 static int launch_generic(const double* src, double* dst, int ni, int nj, int kfirst, int klast,
@@ -448,6 +505,25 @@ int sb_device_count(void) {
 }
 
 int sb_max_depth(void) { return 8; }
+
+int sb_jacobi_schedule(int sweeps, int64_t ni, int64_t nj, int64_t k_out_lo, int64_t k_out_hi,
+                       int ctas, int32_t* items, int64_t cap, int64_t* count, int32_t* dims) {
+    clear_error();
+    int rc = check_dims(ni, nj, std::max<int64_t>(1, k_out_hi));
+    if (rc) return rc;
+    if (sweeps < 1 || sweeps > sb_max_depth())
+        return fail(SB_ERR_PLAN, "sweeps per block must be in [1, %d], got %d", sb_max_depth(), sweeps);
+    if (ni % 2) return fail(SB_ERR_PLAN, "odd ni runs the generic sweep kernel (no tiled items)");
+    if (k_out_lo < 1 || k_out_hi <= k_out_lo)
+        return fail(SB_ERR_ARGUMENT, "bad plane range [%lld, %lld)", (long long)k_out_lo,
+                    (long long)k_out_hi);
+    if (ctas < 1) return fail(SB_ERR_ARGUMENT, "ctas must be >= 1");
+    if (!count || (cap > 0 && !items)) return fail(SB_ERR_ARGUMENT, "null pointer");
+    return with_cfg(sweeps, [&](auto cfg) {
+        return schedule_query<decltype(cfg)>((int)ni, (int)nj, (int)k_out_lo, (int)k_out_hi, ctas,
+                                             items, cap, count, dims);
+    });
+}
 
 int sb_jacobi(double* grid, double* scratch, int64_t ni, int64_t nj, int64_t nk, int64_t iters,
               double a, double b, int depth, void* stream, int* result_in_scratch) {

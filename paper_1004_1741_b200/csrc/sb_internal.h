@@ -25,6 +25,8 @@ int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int ke
 // work schedules of the temporally blocked Jacobi launch (sched.cu)
 int64_t schedule_span(int T, int tiles, int nkout, int grid, int kb);
 int pick_kblock(int T, int tiles, int nkout, int grid);
+std::vector<int4> build_item_list(int T, int tiles_i, int tiles_j, const std::vector<char>& border,
+                                  int kfirst, int klast, int grid, int kb);
 int item_list(int T, int tiles_i, int tiles_j, const std::vector<char>& border, int kfirst,
               int klast, int grid, int kb, const int4** out, int* count);
 

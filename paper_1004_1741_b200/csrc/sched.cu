@@ -168,6 +168,50 @@ static std::vector<Item> build_list(int mode, int T, int tiles_i, int tiles_j,
     return items;
 }
 
+// The explicit list for this launch shape, or empty when the regular
+// k-block decomposition (block length kb) is at least as good under the
+// model.  Host only; deterministic.
+std::vector<int4> build_item_list(int T, int tiles_i, int tiles_j, const std::vector<char>& border,
+                                  int kfirst, int klast, int grid, int kb) {
+    const int mode = env_int("SB_LIST", 1);
+    if (T < 3 || mode == 0 || klast <= kfirst) return {};
+    const int tiles = tiles_i * tiles_j, nk = klast - kfirst;
+    const double f = env_double("SB_SELF", 1.2);
+    // the regular schedule under the same (border-aware) model
+    std::vector<Item> reg;
+    for (int k0 = kfirst; k0 < klast; k0 += kb)
+        for (int t = 0; t < tiles; ++t) {
+            const int k1 = std::min(k0 + kb, klast);
+            reg.push_back({t, k0, k1, (k1 - k0 + 2.0 * T + 4.0) * (border[t] ? f : 1.0)});
+        }
+    double best_span = span_of(reg, grid);
+    std::vector<Item> best;
+    std::vector<int> params;
+    if (mode == 1) {
+        const int m = env_int("SB_LIST_M", 0);
+        if (m > 0) params.push_back(m);
+        else params = {1, 2, 3, 4, 6, 8};
+    } else {
+        const int k = env_int("SB_LIST_KB", 0);
+        if (k > 0) params.push_back(k);
+        else
+            for (int nb = 1; nb <= 32; ++nb) params.push_back((nk + nb - 1) / nb);
+    }
+    const bool force = getenv("SB_LIST_FORCE") != nullptr;
+    for (int prm : params) {
+        std::vector<Item> v = build_list(mode, T, tiles_i, tiles_j, border, kfirst, klast, grid, prm);
+        if (v.empty()) continue;
+        const double sp = span_of(v, grid);
+        if (sp < best_span || (force && best.empty())) {
+            best_span = sp;
+            best.swap(v);
+        }
+    }
+    std::vector<int4> h;
+    for (const Item& x : best) h.push_back(make_int4(x.tile, x.k0, x.k1, 0));
+    return h;
+}
+
 int item_list(int T, int tiles_i, int tiles_j, const std::vector<char>& border, int kfirst,
               int klast, int grid, int kb, const int4** out, int* count) {
     *out = nullptr;
@@ -185,48 +229,16 @@ int item_list(int T, int tiles_i, int tiles_j, const std::vector<char>& border, 
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
     if (it == cache.end()) {
-        const int tiles = tiles_i * tiles_j, nk = klast - kfirst;
-        const double f = env_double("SB_SELF", 1.2);
-        // the regular schedule under the same (border-aware) model
-        std::vector<Item> reg;
-        for (int k0 = kfirst; k0 < klast; k0 += kb)
-            for (int t = 0; t < tiles; ++t) {
-                const int k1 = std::min(k0 + kb, klast);
-                reg.push_back({t, k0, k1, (k1 - k0 + 2.0 * T + 4.0) * (border[t] ? f : 1.0)});
-            }
-        double best_span = span_of(reg, grid);
-        std::vector<Item> best;
-        std::vector<int> params;
-        if (mode == 1) {
-            const int m = env_int("SB_LIST_M", 0);
-            if (m > 0) params.push_back(m);
-            else params = {1, 2, 3, 4, 6, 8};
-        } else {
-            const int k = env_int("SB_LIST_KB", 0);
-            if (k > 0) params.push_back(k);
-            else
-                for (int nb = 1; nb <= 32; ++nb) params.push_back((nk + nb - 1) / nb);
-        }
-        const bool force = getenv("SB_LIST_FORCE") != nullptr;
-        for (int prm : params) {
-            std::vector<Item> v = build_list(mode, T, tiles_i, tiles_j, border, kfirst, klast, grid, prm);
-            if (v.empty()) continue;
-            const double sp = span_of(v, grid);
-            if (sp < best_span || (force && best.empty())) {
-                best_span = sp;
-                best.swap(v);
-            }
-        }
+        const std::vector<int4> h =
+            build_item_list(T, tiles_i, tiles_j, border, kfirst, klast, grid, kb);
         int4* d = nullptr;
-        if (!best.empty()) {
-            std::vector<int4> h;
-            for (const Item& x : best) h.push_back(make_int4(x.tile, x.k0, x.k1, 0));
+        if (!h.empty()) {
             e = cudaMalloc(&d, h.size() * sizeof(int4));
             if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(item list)");
             e = cudaMemcpy(d, h.data(), h.size() * sizeof(int4), cudaMemcpyHostToDevice);
             if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(item list)");
         }
-        it = cache.emplace(key, std::make_pair(d, (int)best.size())).first;
+        it = cache.emplace(key, std::make_pair(d, (int)h.size())).first;
     }
     *out = it->second.first;
     *count = it->second.second;

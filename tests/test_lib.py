@@ -77,3 +77,58 @@ def test_slab_layout_matches_partition_blocks():
             assert (lo.value - 1, hi.value - 1) == ranges[s]
             assert gl.value == (1 if s == 0 else depth)
             assert gh.value == (1 if s == n - 1 else depth)
+
+
+# ---------------------------------------------------------------------------
+# work schedule of the fused Jacobi launch (sb_jacobi_schedule, host only)
+
+@pytest.mark.parametrize("sweeps,ni,nj,k_lo,k_hi,ctas", [
+    (4, 1024, 1024, 1, 1025, 148),   # headline: whole-k bulk rounds + k-piece tail
+    (3, 1024, 1024, 1, 1025, 148),
+    (4, 512, 512, 1, 513, 148),
+    (4, 128, 128, 1, 129, 148),      # fewer tiles than CTAs
+    (4, 1024, 1024, 5, 1021, 148),   # a slab interior (sb_jacobi_planes)
+    (4, 1024, 1024, 1, 5, 148),      # a slab edge
+    (2, 1024, 1024, 1, 1025, 148),   # HBM-bound depths: regular k-blocks
+    (1, 512, 256, 1, 300, 132),
+    (8, 512, 512, 9, 505, 148),
+    (4, 70, 1000, 1, 77, 7),
+])
+def test_schedule_covers_every_tile_plane_once(sweeps, ni, nj, k_lo, k_hi, ctas):
+    import numpy as np
+
+    items, (to, tj, ti_n, tj_n) = _lib.jacobi_schedule(sweeps, ni, nj, k_lo, k_hi, ctas)
+    # the tiles cover the interior [1, ni] x [1, nj]
+    assert to * ti_n >= ni + 1 and to * (ti_n - 1) < ni + 1
+    assert tj * tj_n >= nj and tj * (tj_n - 1) < nj
+    cover = np.zeros((tj_n, ti_n, k_hi - k_lo), dtype=np.int32)
+    for ti, tjj, k0, k1 in items:
+        assert 0 <= ti < ti_n and 0 <= tjj < tj_n and k_lo <= k0 < k1 <= k_hi
+        cover[tjj, ti, k0 - k_lo:k1 - k_lo] += 1
+    assert cover.min() == 1 and cover.max() == 1
+
+
+def test_schedule_headline_uses_whole_k_border_first_list():
+    import numpy as np
+
+    items, (to, tj, ti_n, tj_n) = _lib.jacobi_schedule(4, 1024, 1024, 1, 1025, 148)
+    assert (to, tj, ti_n, tj_n) == (56, 26, 19, 40)
+    full = (items[:, 2] == 1) & (items[:, 3] == 1025)
+    nbulk = (ti_n * tj_n // 148) * 148
+    assert full[:nbulk].all() and not full[nbulk:].any()
+    # border tiles (SEL steps) are claimed first
+    border = (items[:, 0] == 0) | (items[:, 0] == ti_n - 1) | (items[:, 1] == 0) | \
+             (items[:, 1] == tj_n - 1)
+    nb = int(np.count_nonzero(border[:nbulk]))
+    assert border[:nb].all()
+
+
+def test_schedule_rejects_bad_arguments():
+    lib = _lib.load()
+    n = ctypes.c_int64(0)
+    assert lib.sb_jacobi_schedule(9, 64, 64, 1, 9, 148, None, 0, ctypes.byref(n), None) != 0
+    assert lib.sb_jacobi_schedule(4, 63, 64, 1, 9, 148, None, 0, ctypes.byref(n), None) != 0
+    assert lib.sb_jacobi_schedule(4, 64, 64, 5, 5, 148, None, 0, ctypes.byref(n), None) != 0
+    assert lib.sb_jacobi_schedule(4, 64, 64, 1, 9, 0, None, 0, ctypes.byref(n), None) != 0
+    assert lib.sb_jacobi_schedule(4, 64, 64, 1, 9, 148, None, 0, ctypes.byref(n), None) == 0
+    assert n.value > 0
