@@ -223,7 +223,28 @@ def time_jacobi_depths(torch, lib, n, iters, depths):
             best = sec if best is None else min(best, sec)
         mlups = iters * n ** 3 / best / 1e6
         out[f"T{d}"] = {"mlups": mlups, "ms": best * 1e3,
+                        "sweeps_fused_per_pass": min(d, 4),
                         "x_single_sweep_roofline": mlups * 1e6 * 16 / (PEAKS["hbm_gbs"] * 1e9)}
+    # sb_jacobi fuses at most 4 sweeps per pass (deeper requests run as
+    # 4-sweep passes: the fastest on B200).  The genuinely 8-deep kernel (the
+    # slab path's ghost-zone block, sb_jacobi_planes) over the whole grid:
+    sweeps = 8 * (iters // 8)
+    bufs = (g, s)
+    for rep in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for k in range(sweeps // 8):
+            _lib.check(lib.sb_jacobi_planes(bufs[k % 2].data_ptr(), bufs[(k + 1) % 2].data_ptr(),
+                                            n, n, n, 1, n + 1, 8, 0.0, 1 / 6, sp))
+        e1.record(st)
+        _lib.check(lib.sb_sync(sp))
+        sec = e0.elapsed_time(e1) / 1e3
+        if rep:  # first repetition warms up
+            best8 = sec if rep == 1 else min(best8, sec)
+    mlups = sweeps * n ** 3 / best8 / 1e6
+    out["T8_fused"] = {"mlups": mlups, "ms": best8 * 1e3, "sweeps": sweeps,
+                       "sweeps_fused_per_pass": 8,
+                       "x_single_sweep_roofline": mlups * 1e6 * 16 / (PEAKS["hbm_gbs"] * 1e9)}
     return out
 
 
