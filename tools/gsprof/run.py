@@ -5,7 +5,7 @@ import torch
 lib = ctypes.CDLL(str(Path(__file__).resolve().parent / "libsb200_prof.so"))
 lib.sb_gs.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_int, ctypes.c_void_p]
 lib.sb_gs_profile.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
-for (n, nj, nk, it) in [(512, 16, 16, 4), (512, 512, 16, 2), (512, 512, 512, 16)]:
+for (n, nj, nk, it) in [(512, 512, 512, 20)]:
     g = torch.rand((nk + 2, nj + 2, n + 2), dtype=torch.float64, device="cuda")
     lib.sb_gs(g.data_ptr(), n, nj, nk, 1, 1/6, 1, None); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
