@@ -183,12 +183,21 @@ __device__ void gs_loader(const CUtensorMap* ld_map, const GsParams& p, double* 
     uint32_t gload = 0;
     int lq = 0;
     long long t0 = clock64();
+#ifdef SB_GS_PROFILE
+    unsigned long long l_empty = 0, l_deps = 0;
+#endif
     while (true) {
         const GsTask lt = decode_task<C>(p, atomicAdd(p.ticket, 1));
         queue[lq] = lt;  // published to the other warps by the next full[] phase
         lq = (lq + 1) % C::QS;
         const uint32_t slot0 = gload % NS;
         if (lt.s < 0) {
+#ifdef SB_GS_PROFILE
+            if (p.prof) {
+                atomicAdd(&p.prof[4], l_empty);
+                atomicAdd(&p.prof[5], l_deps);
+            }
+#endif
             // release the compute warps waiting for this (stop) task's first
             // chunk: complete that slot's barrier phase without data
             if (gload >= NS) mbar_wait(&empty[slot0], ((gload - NS) / NS) & 1);
@@ -199,11 +208,21 @@ __device__ void gs_loader(const CUtensorMap* ld_map, const GsParams& p, double* 
         deps_init<C>(p, lt, deps);
         for (int c = 0; c < nch; ++c, ++gload) {
             const uint32_t slot = gload % NS;
+#ifdef SB_GS_PROFILE
+            long long ta = clock64();
+#endif
             if (gload >= NS) {  // the slot's previous chunk must have been stored
                 while (!mbar_try_wait(&empty[slot], ((gload - NS) / NS) & 1)) gs_check_abort(p, t0);
             }
+#ifdef SB_GS_PROFILE
+            long long tb = clock64();
+            l_empty += tb - ta;
+#endif
             while (!((c > 0 || prog_ready<C>(p, lt.s - (C::R - 1), lt.tile, nch)) && deps_ready(deps, c)))
                 gs_check_abort(p, t0);
+#ifdef SB_GS_PROFILE
+            l_deps += clock64() - tb;
+#endif
             t0 = clock64();
             fence_proxy_async_global();
             mbar_arrive_expect_tx(&full[slot], C::BOX_BYTES);
@@ -499,7 +518,7 @@ static GsScratch g_gs[16];
 static unsigned long long* g_gs_prof = nullptr;
 extern "C" void sb_gs_profile(unsigned long long* out) {
     cudaDeviceSynchronize();
-    if (g_gs_prof) cudaMemcpy(out, g_gs_prof, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    if (g_gs_prof) cudaMemcpy(out, g_gs_prof, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
 }
 #endif
 

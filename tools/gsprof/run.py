@@ -10,7 +10,8 @@ for (n, nj, nk, it) in [(512, 512, 512, 20)]:
     lib.sb_gs(g.data_ptr(), n, nj, nk, 1, 1/6, 1, None); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); rc = lib.sb_gs(g.data_ptr(), n, nj, nk, it, 1/6, 1, None); e1.record(); torch.cuda.synchronize()
-    out = (ctypes.c_ulonglong * 4)(); lib.sb_gs_profile(out)
-    tot, ws, wc, nt = list(out)
+    out = (ctypes.c_ulonglong * 6)(); lib.sb_gs_profile(out)
+    tot, ws, wc, nt, le, ld = list(out)
     print(f"{n}x{nj}x{nk}x{it}: {e0.elapsed_time(e1):.3f} ms rc={rc}; per-CTA cycles total {tot/148:.3g}; "
-          f"wait task-start {100*ws/tot:.1f}%, wait chunk {100*wc/tot:.1f}%, tasks {nt}", flush=True)
+          f"wait task-start {100*ws/tot:.1f}%, wait chunk {100*wc/tot:.1f}%, tasks {nt}; "
+          f"loader: waiting for a free slot {100*le/tot:.2f}% ({le:.3g} cyc), for dependencies {100*ld/tot:.2f}% ({ld:.3g})", flush=True)
