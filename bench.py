@@ -342,8 +342,8 @@ def run_gpu_arm(args):
     # e2e through the public C-ABI host-buffer entry point: every step one
     # grid goes pinned host -> H2D -> SWEEPS sweeps -> D2H.  At N=1 the steps
     # go through sb_run_host_batch, which overlaps step i's upload with step
-    # i-1's sweeps and step i-2's download (two pinned host grids alternate:
-    # step i starts from step i-2's result).
+    # i-1's sweeps and step i-2's download (three pinned host grids rotate:
+    # step i starts from step i-3's result).
     e2e = None
     if not args.no_e2e:
         host = _lib.pinned_array(tuple(eng.bufs[0].shape))
@@ -351,12 +351,14 @@ def run_gpu_arm(args):
         if world == 1:
             host2 = _lib.pinned_array(tuple(eng.bufs[0].shape))
             host2[...] = host
+            host3 = _lib.pinned_array(tuple(eng.bufs[0].shape))
+            host3[...] = host
             nbytes = host.nbytes
-            ptrs = [host.ctypes.data, host2.ctypes.data]
-            warm = (ctypes.c_void_p * 2)(*ptrs)
-            _lib.check(lib.sb_run_host_batch(0, warm, 2, NI, NJ, NK_PER_GPU, depth, 0.0, 1 / 6,
+            ptrs = [host.ctypes.data, host2.ctypes.data, host3.ctypes.data]
+            warm = (ctypes.c_void_p * 3)(*ptrs)
+            _lib.check(lib.sb_run_host_batch(0, warm, 3, NI, NJ, NK_PER_GPU, depth, 0.0, 1 / 6,
                                              depth, local))  # allocate + warm
-            seq = (ctypes.c_void_p * args.steps)(*[ptrs[i % 2] for i in range(args.steps)])
+            seq = (ctypes.c_void_p * args.steps)(*[ptrs[i % 3] for i in range(args.steps)])
             t0 = time.perf_counter()
             _lib.check(lib.sb_run_host_batch(0, seq, args.steps, NI, NJ, NK_PER_GPU, SWEEPS, 0.0,
                                              1 / 6, depth, local))
@@ -365,7 +367,7 @@ def run_gpu_arm(args):
                    "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                    "path": "sb_run_host_batch (C ABI; pinned host grids; per step H2D + sweeps "
                            "+ D2H inside the timed region, consecutive steps overlapped)"}
-            del host2
+            del host2, host3
         else:
             e2e = run_e2e_multi(torch, dist, eng, host, args, dev, st, world)
         del host

@@ -169,12 +169,13 @@ int sb_run_host(int kernel, double* host_grid, int64_t ni, int64_t nj, int64_t n
  * Batch form of sb_run_host for a stream of independent grids of one shape
  * (the reference's perf.measure runs fresh inputs back to back): entry i's
  * host->device copy overlaps entry i-1's sweeps and entry i-2's
- * device->host copy, so with pinned grids the batch moves at
- * max(H2D, sweeps, D2H) per grid.  Entries are processed in order; an entry
- * may repeat the pointer of an entry at least two places earlier and then
- * starts from that entry's result; adjacent repeats -> SB_ERR_ARGUMENT.
- * Synchronous; every grid is updated in place.  Uses two device slots
- * (Jacobi: four grids' worth of device memory).
+ * device->host copy (PCIe is full duplex), so with pinned grids the batch
+ * moves at about max(H2D, sweeps, D2H) per grid.  Entries are processed in
+ * order; an entry may repeat the pointer of an entry at least two places
+ * earlier and then starts from that entry's result (its upload waits for
+ * that download); adjacent repeats -> SB_ERR_ARGUMENT.  Synchronous; every
+ * grid is updated in place.  Uses three device slots (Jacobi: six grids'
+ * worth of device memory), two if the third does not fit.
  */
 int sb_run_host_batch(int kernel, double* const* host_grids, int count, int64_t ni, int64_t nj,
                       int64_t nk, int64_t iters, double a, double b, int depth, int device);

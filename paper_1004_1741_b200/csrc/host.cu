@@ -115,19 +115,27 @@ int sb_run_host(int kernel, double* host_grid, int64_t ni, int64_t nj, int64_t n
 // sum.  Ordering: D2H(i) completes before H2D(i+2) starts (same slot), so an
 // entry may repeat the pointer of an entry >= 2 places earlier and then starts
 // from that entry's result; adjacent repeats are rejected.
+// Device slots of the batch pipeline.  Three slots let entry i+1's upload
+// run during entry i's sweeps while entry i-1 downloads (PCIe Gen5 is full
+// duplex: 55.6 GB/s up, 53.9 down, 94.6 together on B200), so a batch moves
+// at about max(H2D, sweeps, D2H, duplex) per grid; two slots (if memory is
+// short) serialise each upload behind the download two entries back.
+constexpr int kBatchSlots = 3;
 struct BatchCtx {
-    double* g[2] = {nullptr, nullptr};
-    double* s[2] = {nullptr, nullptr};
+    double* g[kBatchSlots] = {};
+    double* s[kBatchSlots] = {};
+    int nslots = 0;
     size_t cap = 0;
     bool two = false;
     cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // H2D, sweeps, D2H
-    cudaEvent_t up[2], done[2], down[2];
+    cudaEvent_t up[kBatchSlots], done[kBatchSlots], down[kBatchSlots];
     bool ev = false;
 };
 static BatchCtx g_batch[64];
 
 static void batch_free(BatchCtx& B) {
-    for (int i = 0; i < 2; ++i) {
+    B.nslots = 0;
+    for (int i = 0; i < kBatchSlots; ++i) {
         if (B.g[i]) cudaFree(B.g[i]);
         if (B.s[i]) cudaFree(B.s[i]);
         B.g[i] = B.s[i] = nullptr;
@@ -170,7 +178,7 @@ int sb_run_host_batch(int kernel, double* const* host_grids, int count, int64_t 
                 return cuda_fail(e, "cudaStreamCreate");
     }
     if (!B.ev) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kBatchSlots; ++i) {
             if ((e = cudaEventCreateWithFlags(&B.up[i], cudaEventDisableTiming)) != cudaSuccess ||
                 (e = cudaEventCreateWithFlags(&B.done[i], cudaEventDisableTiming)) != cudaSuccess ||
                 (e = cudaEventCreateWithFlags(&B.down[i], cudaEventDisableTiming)) != cudaSuccess)
@@ -180,21 +188,38 @@ int sb_run_host_batch(int kernel, double* const* host_grids, int count, int64_t 
     }
     if (B.cap < cells || (two && !B.two)) {
         batch_free(B);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kBatchSlots; ++i) {
             if ((e = cudaMalloc(&B.g[i], bytes)) != cudaSuccess ||
                 (two && (e = cudaMalloc(&B.s[i], bytes)) != cudaSuccess)) {
+                cudaGetLastError();
+                if (i >= 2) break;  // two slots still pipeline
                 batch_free(B);
                 return cuda_fail(e, "cudaMalloc(batch slots)");
             }
+            B.nslots = i + 1;
+        }
+        if (B.nslots < kBatchSlots) {  // drop a half-allocated slot
+            const int i = B.nslots;
+            if (B.g[i]) cudaFree(B.g[i]);
+            if (B.s[i]) cudaFree(B.s[i]);
+            B.g[i] = B.s[i] = nullptr;
         }
         B.cap = cells;
         B.two = two;
     }
+    const int ns = B.nslots;
     cudaStream_t h2d = B.st[0], comp = B.st[1], d2h = B.st[2];
     for (int i = 0; i < count; ++i) {
-        const int sl = i & 1;
-        if (i >= 2 && (e = cudaStreamWaitEvent(h2d, B.down[sl], 0)) != cudaSuccess)
+        const int sl = i % ns;
+        // the slot's previous entry has been downloaded
+        if (i >= ns && (e = cudaStreamWaitEvent(h2d, B.down[sl], 0)) != cudaSuccess)
             return cuda_fail(e, "cudaStreamWaitEvent");
+        // an entry repeating the grid of an entry still in flight starts from
+        // that entry's result (entries up to i-ns are already ordered above)
+        for (int j = std::max(0, i - ns + 1); j < i; ++j)
+            if (host_grids[j] == host_grids[i] &&
+                (e = cudaStreamWaitEvent(h2d, B.down[j % ns], 0)) != cudaSuccess)
+                return cuda_fail(e, "cudaStreamWaitEvent");
         if ((e = cudaMemcpyAsync(B.g[sl], host_grids[i], bytes, cudaMemcpyHostToDevice, h2d)) !=
                 cudaSuccess ||
             (e = cudaEventRecord(B.up[sl], h2d)) != cudaSuccess ||
