@@ -503,7 +503,12 @@ __global__ void gs_serial_kernel(double* g, int ni, int nj, int nk, int sweeps, 
 }
 
 // ---------------------------------------------------------------------------
-using GsC = GsCfg<16, 16, 16, 5, 1>;  // CW = 16: 128-B lines (TMA smem addresses must be 128-B aligned)
+// 16 x 6-line tiles with 4-slot rings: 74 KB of shared memory, three CTAs per
+// SM.  The resident CTAs hide each other's chunk waits and barriers (one
+// 16 x 16 CTA per SM, 5 slots: 239.5 GLUP/s at 512^3 x 100; 16 x 8, two per
+// SM: 245.7; 16 x 6, three per SM: 248.8; 16 x 4, four: 236.4; 8 x 12: 237).
+using GsC = GsCfg<16, 6, 16, 4, 1>;
+using GsC1 = GsCfg<16, 16, 16, 5, 1>;  // one CTA per SM (SB_GSCFG=1)
 
 struct GsScratch {
     int* words = nullptr;  // ticket, err
@@ -668,7 +673,10 @@ int gs_serial_run(double* grid, int ni, int nj, int nk, int64_t iters, double b,
 int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,
            cudaStream_t st) {
     if (!tma_ok(grid, ni)) return gs_serial_run(grid, ni, nj, nk, iters, b, kernel, st);
-    return gs_launch<GsC>(grid, ni, nj, nk, iters, b, kernel == SB_KERNEL_GS_INTERLEAVED, st);
+    static const int v = getenv("SB_GSCFG") ? atoi(getenv("SB_GSCFG")) : 0;  // tuning
+    const bool inter = kernel == SB_KERNEL_GS_INTERLEAVED;
+    if (v == 1) return gs_launch<GsC1>(grid, ni, nj, nk, iters, b, inter, st);
+    return gs_launch<GsC>(grid, ni, nj, nk, iters, b, inter, st);
 }
 
 int gs_serial_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,
