@@ -123,51 +123,87 @@ def synth_slab(torch, eng, dev):
     return x
 
 
-def cpu_reference_rate(budget_s=12.0, n=512, threads=None):
+def cpu_sample_n():
+    """Grid edge for the CPU samples: the headline's 1024^3 when the host has
+    room for it (two 8.6 GB grids plus headroom), else 512^3."""
+    try:
+        import psutil
+
+        if psutil.virtual_memory().available > 64e9:
+            return 1024
+    except Exception:  # noqa: BLE001
+        pass
+    return 512
+
+
+def cpu_grid(n):
+    import numpy as np
+
+    g = np.random.default_rng(42).random((n + 2, n + 2, n + 2))
+    g[0], g[-1], g[:, 0], g[:, -1], g[:, :, 0], g[:, :, -1] = 0, 0, 0, 0, 0, 0
+    return g
+
+
+def cpu_reference_rate(budget_s=12.0, n=None, threads=None, g=None, sweeps=None):
     """The reference's CPU path (oracle port of the threaded k-slab Jacobi
     engine, reference sweeps/threaded.py:28-59) on the host cores: a bounded
     sample of the workload (n^3 interior, S sweeps sized to ~budget_s)."""
-    import numpy as np
-
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle  # CPU baseline only
 
     threads = threads or os.cpu_count() or 1
-    g = np.random.default_rng(42).random((n + 2, n + 2, n + 2))
-    g[0], g[-1], g[:, 0], g[:, -1], g[:, :, 0], g[:, :, -1] = 0, 0, 0, 0, 0, 0
-    t0 = time.perf_counter()
-    oracle.run_threaded("jacobi", g, 2, 0.0, 1 / 6, threads=threads)
-    calib = (time.perf_counter() - t0) / 2
-    sweeps = int(max(2, min(200, budget_s / max(calib, 1e-6))))
-    t0 = time.perf_counter()
-    oracle.run_threaded("jacobi", g, sweeps, 0.0, 1 / 6, threads=threads)
-    sec = time.perf_counter() - t0
+    if g is None:
+        n = n or cpu_sample_n()
+        g = cpu_grid(n)
+    n = g.shape[0] - 2
+    if sweeps is None:
+        calib = oracle.time_threaded_jacobi(g, 2, 0.0, 1 / 6, threads=threads) / 2
+        sweeps = int(max(2, min(200, budget_s / max(calib, 1e-6))))
+    sec = oracle.time_threaded_jacobi(g, sweeps, 0.0, 1 / 6, threads=threads)
     return {"value": sweeps * n ** 3 / sec / 1e6, "unit": "MLUP/s", "cores": threads,
             "kind": "port",
-            "sample": f"{n}^3 interior, {sweeps} Jacobi sweeps, oracle port of the reference's "
-                      f"threaded k-slab engine on {threads} host threads"}
+            "sample": f"{n}^3 interior, {sweeps} Jacobi sweeps (sweep time only; grid copy and "
+                      f"scratch allocated beforehand), oracle port of the reference's threaded "
+                      f"k-slab engine on {threads} host threads"}
+
+
+def arm_config(world, depth):
+    """The workload description both arms report (GPU arm and --impl reference)."""
+    return {"workload": "BASELINE cfg4 weak: Jacobi 1024x1024x(1024*N), 100 sweeps/step, "
+                        "z-slabs + halo exchange",
+            "ni": NI, "nj": NJ, "nk": NK_PER_GPU * world, "sweeps_per_step": SWEEPS,
+            "depth": depth, "coeffs": [0.0, 1 / 6],
+            "parallelism": f"z-slabs x{world}" if world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (8.6 GB/GPU per buffer)"}
 
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference_arm(args):
+    """The reference's CPU implementation of the path (the oracle port of its
+    threaded engine; the reference package is Python/numba and is not on the
+    GPU box) on all host threads, on this arm's config and metric: each step
+    times a bounded sample of the workload (the headline grid when it fits
+    in host memory, S sweeps sized so the run ends within minutes)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    n = 512
-    rates, secs = [], []
-    budget = max(5.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    g = cpu_grid(cpu_sample_n())
+    rates = []
+    budget = max(4.0, min(15.0, 120.0 / max(1, args.steps + args.warmup)))
+    r = cpu_reference_rate(budget_s=budget, g=g)  # calibrates the sample's sweep count
+    sweeps = int(r["sample"].split(" Jacobi sweeps")[0].split()[-1])
     for step in range(args.warmup + args.steps):
-        r = cpu_reference_rate(budget_s=budget, n=n)
+        r = cpu_reference_rate(g=g, sweeps=sweeps)
         if step >= args.warmup:
             rates.append(r["value"])
-            secs.append(budget)
     value = statistics.median(rates)
+    cfg = arm_config(world, args.depth)
+    cfg["cpu_sample"] = r["sample"]
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "MLUP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "cfg4-weak Jacobi (bounded CPU sample: 512^3 x S sweeps per step)",
-                       "sample_n": n, "parallelism": f"{os.cpu_count()} host threads"},
+            "config": cfg,
             "cpu_baseline": dict(r, value=value),
             "e2e": {"value": value, "unit": "MLUP/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -388,12 +424,7 @@ def run_gpu_arm(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec / args.steps * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (deterministic sin-hash field in [0,1), zero Dirichlet halo)",
-                "config": {"workload": "BASELINE cfg4 weak: Jacobi 1024x1024x(1024*N), "
-                                       "100 sweeps/step, z-slabs + halo exchange",
-                           "ni": NI, "nj": NJ, "nk": nk_total, "sweeps_per_step": SWEEPS,
-                           "depth": depth, "coeffs": [0.0, 1 / 6],
-                           "parallelism": f"z-slabs x{world}" if world > 1 else "1 GPU",
-                           "l2": "inputs larger than L2 (8.6 GB/GPU per buffer)"},
+                "config": arm_config(world, depth),
                 "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "clocks": clk.summary(), "also": also}
         print(json.dumps(line), flush=True)

@@ -91,6 +91,29 @@ def run_threaded(kernel, data, iters, a=0.0, b=1.0 / 6.0, threads=None):
     return g
 
 
+def time_threaded_jacobi(data, iters, a=0.0, b=1.0 / 6.0, threads=None):
+    """Seconds spent in `iters` threaded Jacobi sweeps of `data` (k-slabs,
+    reference threaded.py:28-59), excluding the setup: the working copy and
+    the scratch grid are allocated and touched first, so a short bounded
+    sample measures the sweep rate rather than page faults (CPU baseline of
+    bench.py)."""
+    import time
+
+    threads = threads or os.cpu_count() or 1
+    g = np.array(data, dtype=np.float64, order="C", copy=True)
+    ni, nj, nk = _check(g)
+    scratch = g.copy()
+    lib = load()
+    threads = max(1, min(threads, nk))
+    t0 = time.perf_counter()
+    in_s = lib.sbo_run_threaded_jacobi(g.ctypes.data, scratch.ctypes.data, ni, nj, nk, iters, a, b,
+                                       threads)
+    sec = time.perf_counter() - t0
+    if in_s < 0:
+        raise ValueError("partition error")
+    return sec
+
+
 def gs_line(kernel, data, k, j, b):
     """One in-place GS line update of interior line (k, j) (reference
     kernels.py:236-247 via the window kernels).  Returns a new array."""
