@@ -383,7 +383,7 @@ def run_gpu_arm(args):
     e2e = None
     if not args.no_e2e:
         host = _lib.pinned_array(tuple(eng.bufs[0].shape))
-        host[...] = eng.bufs[eng.cur].cpu().numpy()
+        torch.from_numpy(host).copy_(eng.bufs[eng.cur])  # no pageable temporary
         if world == 1 and args.e2e_path == "batch":
             host2 = _lib.pinned_array(tuple(eng.bufs[0].shape))
             host2[...] = host
@@ -442,7 +442,16 @@ def run_e2e_engine(torch, dist, eng, host_in, args, dev, world):
     full duplex).  Timed as the max over ranks."""
     nbytes = host_in.nbytes
     src = torch.from_numpy(host_in)
-    host_out = _lib_pinned(host_in.shape)
+    # a second pinned slab for the downloads when the host has room for one
+    # per rank (all ranks of the node allocate at once); else the downloads
+    # go back into the input slab and each upload waits for the previous one
+    try:
+        import psutil
+
+        roomy = psutil.virtual_memory().available > 3 * nbytes * int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    except Exception:  # noqa: BLE001
+        roomy = False
+    host_out = _lib_pinned(host_in.shape) if roomy else host_in
     out = torch.from_numpy(host_out)
     stage = [torch.empty_like(eng.bufs[0]) for _ in range(2)]
     res = [torch.empty_like(eng.bufs[0]) for _ in range(2)]
@@ -458,6 +467,8 @@ def run_e2e_engine(torch, dist, eng, host_in, args, dev, world):
         k = i % 2
         if i >= 2:
             up_s.wait_event(ev_free[k])
+        if not roomy and i >= 1:
+            up_s.wait_event(ev_dn[(i - 1) % 2])  # the shared slab's previous download
         with torch.cuda.stream(up_s):
             stage[k].copy_(src, non_blocking=True)
         ev_up[k].record(up_s)
