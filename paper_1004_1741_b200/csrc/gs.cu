@@ -554,7 +554,7 @@ static std::vector<int2> wavefront_order(int tiles_j, int tiles_k, int sweeps, i
 }
 
 static int gs_window() {
-    static int w = getenv("SB_GS_WINDOW") ? std::max(1, atoi(getenv("SB_GS_WINDOW"))) : 4;
+    static int w = getenv("SB_GS_WINDOW") ? std::max(1, atoi(getenv("SB_GS_WINDOW"))) : 3;
     return w;
 }
 
