@@ -116,6 +116,18 @@ def test_run_batch_pipelined_host_path():
         wb = oracle.run_serial(kernel, b0.data, 10, a, b)
         run_batch(plan, [a0, b0, a0, b0])
         assert sha(a0.data) == sha(wa) and sha(b0.data) == sha(wb), kernel
+        # more grids than device slots (three): every slot is reused, and
+        # A, B, C, A, B, C repeats at distance three
+        many = [make_input({"shape": [22, 14, 10], "pattern": "random", "seed": 70 + i,
+                            "lo": -1.0, "hi": 1.0}) for i in range(7)]
+        want = [oracle.run_serial(kernel, g.data, 5, a, b) for g in many]
+        run_batch(plan, many)
+        assert all(sha(g.data) == sha(w) for g, w in zip(many, want)), kernel
+        trio = [make_input({"shape": [22, 14, 10], "pattern": "random", "seed": 80 + i,
+                            "lo": -1.0, "hi": 1.0}) for i in range(3)]
+        want = [oracle.run_serial(kernel, g.data, 10, a, b) for g in trio]
+        run_batch(plan, trio + trio)
+        assert all(sha(g.data) == sha(w) for g, w in zip(trio, want)), kernel
     g = make_input({"shape": [8, 8, 8], "pattern": "random", "seed": 1, "lo": 0.0, "hi": 1.0})
     with pytest.raises(ValueError):
         run_batch(SweepPlan("jacobi", "serial", 1), [g, g])
