@@ -38,10 +38,12 @@
 // cost more issue slots than the two DP operations they save.)  Halo (Dirichlet) cells are never computed: at every level they carry the
 // input value.
 //
-// Work distribution: persistent CTAs grab (tile, k-block) items from a
-// global atomic counter in k-block-major order (CTAs running together hold
-// neighbouring tiles of the same planes, so overlapping halo reads hit L2).
-// The TMA producer runs C::AHEAD planes ahead, across item boundaries.
+// Work distribution: persistent CTAs claim (tile, k-range) items from a
+// global atomic counter -- regular k-block-major items (CTAs running together
+// hold neighbouring tiles of the same planes, so overlapping halo reads hit
+// L2) or an explicit list built on the host (sched.cu: whole-k rounds with
+// the border tiles first, then a balanced tail of k-pieces).  The TMA
+// producer runs C::AHEAD planes ahead, across item boundaries.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
