@@ -298,3 +298,28 @@ def test_full_size_fixed_point(kernel):
     assert bool((out == 1.75).all())
     del g, out
     torch.cuda.empty_cache()
+
+
+def test_special_values_match_the_oracle():
+    """Signed zeros, infinities, NaNs, subnormals and huge values in the
+    field: every cell equals the oracle's bit for bit except NaN payloads
+    (the GPU's default NaN differs from x86's; NaN positions must agree)."""
+    rng = np.random.default_rng(5)
+    base = make_input({"shape": [34, 20, 16], "pattern": "random", "seed": 12, "lo": -1.0,
+                       "hi": 1.0}).data
+    specials = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, -2.2e-308, 1e308, -1e308])
+    data = base.copy()
+    idx = rng.integers(0, data.size, size=60)
+    data.reshape(-1)[idx] = specials[rng.integers(0, specials.size, size=idx.size)]
+    data[1:-1, 1:-1, 1:-1][data[1:-1, 1:-1, 1:-1] == 0.0] = -0.0  # some interior -0.0
+    for kernel, (a, b), depths in (("jacobi", (0.0, 1 / 6), (1, 4)),
+                                   ("jacobi", (0.5, 0.1), (1, 3)),
+                                   ("gs-naive", (0.0, 1 / 6), (1,)),
+                                   ("gs-interleaved", (0.0, 1 / 6), (1,))):
+        want = oracle.run_serial(kernel, data, 3, a, b)
+        for depth in depths:
+            got = run_device(kernel, data, 3, a, b, depth)
+            nan_w, nan_g = np.isnan(want), np.isnan(got)
+            assert np.array_equal(nan_w, nan_g), (kernel, depth)
+            assert np.array_equal(want[~nan_w].view(np.int64), got[~nan_g].view(np.int64)), \
+                (kernel, depth)
