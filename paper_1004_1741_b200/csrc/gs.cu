@@ -53,8 +53,8 @@
 
 namespace sb {
 
-int make_grid_map3(CUtensorMap* m, const double* base, int64_t nip, int64_t njp, int64_t nkp, int bw,
-                   int bh, int bd);
+int make_grid_map3p(CUtensorMap* m, const double* base, int64_t nip, int64_t njp, int64_t nkp,
+                    int bw, int bh, int bd, int64_t pitch);
 
 struct GsParams {
     int ni, nj, nk;
@@ -560,7 +560,7 @@ static int gs_window() {
 
 template <class C>
 static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double b, bool inter,
-                     cudaStream_t st) {
+                     cudaStream_t st, int64_t pitch = 0) {
     int dev;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
@@ -607,8 +607,9 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
 
     CUtensorMap lmap, smap;
     const int64_t nip = ni + 2, njp = nj + 2, nkp = nk + 2;
-    if ((rc = make_grid_map3(&lmap, grid, nip, njp, nkp, C::CW, C::LJ, C::LK))) return rc;
-    if ((rc = make_grid_map3(&smap, grid, nip, njp, nkp, C::CW, C::BJ, 1))) return rc;
+    if (pitch <= 0) pitch = nip;
+    if ((rc = make_grid_map3p(&lmap, grid, nip, njp, nkp, C::CW, C::LJ, C::LK, pitch))) return rc;
+    if ((rc = make_grid_map3p(&smap, grid, nip, njp, nkp, C::CW, C::BJ, 1, pitch))) return rc;
 
     static int occ = -1;
     auto kern_n = gs_tile_kernel<C, false>;
@@ -670,9 +671,60 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
 int gs_serial_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,
                   cudaStream_t st);
 
+// Grids TMA cannot describe directly (odd ni: the row pitch (ni+2)*8 bytes is
+// not a multiple of 16; or a base address that is not 16-byte aligned) run
+// the tile kernel on a pitched copy: rows padded to an even number of doubles
+// (the extra column lies outside the tensor map, so it is never read or
+// written), copied in and out with cudaMemcpy2D.  One scratch buffer per
+// device, grown on demand, stream-ordered like the rest of sb_gs.
+struct GsPitched {
+    double* buf = nullptr;
+    size_t cap = 0;  // doubles
+};
+static GsPitched g_gs_pitched[16];
+
+static int gs_run_pitched(double* grid, int ni, int nj, int nk, int64_t iters, double b,
+                          bool inter, cudaStream_t st) {
+    int dev;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev >= 16) return fail(SB_ERR_CUDA, "device index %d unsupported", dev);
+    GsPitched& P = g_gs_pitched[dev];
+    const int64_t nip = ni + 2, pitch = (nip + 1) / 2 * 2, rows = int64_t(nj + 2) * (nk + 2);
+    const size_t need = size_t(pitch) * size_t(rows);
+    if (P.cap < need) {
+        if (P.buf && (e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "sync");
+        if (P.buf) cudaFree(P.buf);
+        P.buf = nullptr;
+        P.cap = 0;
+        if ((e = cudaMalloc(&P.buf, need * sizeof(double))) != cudaSuccess)
+            return cuda_fail(e, "cudaMalloc(pitched GS grid)");
+        P.cap = need;
+    }
+    if ((e = cudaMemcpy2DAsync(P.buf, pitch * 8, grid, nip * 8, nip * 8, rows,
+                               cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+        return cuda_fail(e, "cudaMemcpy2DAsync(in)");
+    int rc = (iters <= 2)
+                 ? gs_launch<GsC1>(P.buf, ni, nj, nk, iters, b, inter, st, pitch)
+                 : gs_launch<GsC>(P.buf, ni, nj, nk, iters, b, inter, st, pitch);
+    if (rc) return rc;
+    if ((e = cudaMemcpy2DAsync(grid, nip * 8, P.buf, pitch * 8, nip * 8, rows,
+                               cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+        return cuda_fail(e, "cudaMemcpy2DAsync(out)");
+    return SB_OK;
+}
+
 int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,
            cudaStream_t st) {
-    if (!tma_ok(grid, ni)) return gs_serial_run(grid, ni, nj, nk, iters, b, kernel, st);
+    if (!tma_ok(grid, ni)) {
+        // tiny grids: the exact serial kernel is cheaper than the copies
+        if (int64_t(ni) * nj * nk * iters < (int64_t(1) << 16))
+            return gs_serial_run(grid, ni, nj, nk, iters, b, kernel, st);
+        // ni < 2: the interleaved association degenerates to the naive one
+        // (reference kernels.py:168-176)
+        return gs_run_pitched(grid, ni, nj, nk, iters, b,
+                              kernel == SB_KERNEL_GS_INTERLEAVED && ni >= 2, st);
+    }
     static const int v = getenv("SB_GSCFG") ? atoi(getenv("SB_GSCFG")) : 0;  // tuning
     const bool inter = kernel == SB_KERNEL_GS_INTERLEAVED;
     // one or two sweeps per call (the GS z-pipeline's stages): the 16 x 16

@@ -69,13 +69,14 @@ static EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// 3-D map over a padded grid with a (bw, bh, bd) box.
-int make_grid_map3(CUtensorMap* m, const double* base, int64_t nip, int64_t njp, int64_t nkp,
-                   int bw, int bh, int bd) {
+// 3-D map over a padded grid with a (bw, bh, bd) box; rows `pitch` doubles
+// apart (pitch >= nip, even: TMA needs 16-byte row strides).
+int make_grid_map3p(CUtensorMap* m, const double* base, int64_t nip, int64_t njp, int64_t nkp,
+                    int bw, int bh, int bd, int64_t pitch) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return fail(SB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[3] = {(cuuint64_t)nip, (cuuint64_t)njp, (cuuint64_t)nkp};
-    cuuint64_t strides[2] = {(cuuint64_t)(nip * 8), (cuuint64_t)(nip * njp * 8)};
+    cuuint64_t strides[2] = {(cuuint64_t)(pitch * 8), (cuuint64_t)(pitch * njp * 8)};
     cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bd};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
@@ -83,6 +84,11 @@ int make_grid_map3(CUtensorMap* m, const double* base, int64_t nip, int64_t njp,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(SB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return SB_OK;
+}
+
+int make_grid_map3(CUtensorMap* m, const double* base, int64_t nip, int64_t njp, int64_t nkp,
+                   int bw, int bh, int bd) {
+    return make_grid_map3p(m, base, nip, njp, nkp, bw, bh, bd, nip);
 }
 
 int make_grid_map(CUtensorMap* m, const double* base, int64_t nip, int64_t njp, int64_t nkp,

@@ -323,3 +323,17 @@ def test_special_values_match_the_oracle():
             assert np.array_equal(nan_w, nan_g), (kernel, depth)
             assert np.array_equal(want[~nan_w].view(np.int64), got[~nan_g].view(np.int64)), \
                 (kernel, depth)
+
+
+@pytest.mark.parametrize("shape,iters", [((33, 40, 29), 5), ((129, 70, 48), 3), ((1, 130, 90), 4),
+                                         ((255, 37, 20), 2)])
+def test_gs_odd_row_pitch_pitched_path(shape, iters):
+    """Odd ni (row pitch not a multiple of 16 bytes): GS runs the tile kernel
+    on a pitched copy -- bitwise equal to the oracle for both associations
+    (ni = 1: the interleaved form degenerates to the naive one)."""
+    data = make_input({"shape": list(shape), "pattern": "random", "seed": 21, "lo": -1.0,
+                       "hi": 1.0}).data
+    for kernel in ("gs-naive", "gs-interleaved"):
+        want = oracle.run_serial(kernel, data, iters, 0.0, 1 / 6)
+        got = run_device(kernel, data, iters, 0.0, 1 / 6, 1)
+        assert sha(got) == sha(want), (shape, kernel)
