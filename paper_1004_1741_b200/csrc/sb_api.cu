@@ -250,7 +250,7 @@ static TbPlan tb_plan(int ni, int nj, int kfirst, int klast, int grid) {
 
 template <class C, bool AZ>
 static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk, int kfirst,
-                          int klast, double a, double b, cudaStream_t st) {
+                          int klast, double a, double b, cudaStream_t st, int64_t pitch) {
     int* counters;
     int sms;
     int rc = get_counters(&counters, &sms);
@@ -270,9 +270,12 @@ static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk
     }
     CUtensorMap smap, dmap;
     const int64_t nip = ni + 2, njp = nj + 2, nkp = nk + 2;
-    if ((rc = make_grid_map(&smap, src, nip, njp, nkp, C::BW, C::BH))) return rc;
+    if (pitch <= 0) pitch = nip;
+    // without TS the kernel addresses dst directly with the dense pitch
+    if (!C::TS && pitch != nip) return fail(SB_ERR_PLAN, "pitched grids need a TMA-store depth");
+    if ((rc = make_grid_map3p(&smap, src, nip, njp, nkp, C::BW, C::BH, 1, pitch))) return rc;
     if (C::TS) {
-        if ((rc = make_grid_map(&dmap, dst, nip, njp, nkp, C::TO, C::TJ))) return rc;
+        if ((rc = make_grid_map3p(&dmap, dst, nip, njp, nkp, C::TO, C::TJ, 1, pitch))) return rc;
     } else {
         dmap = smap;  // unused
     }
@@ -321,9 +324,10 @@ static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk
 
 template <class C>
 static int launch_tb(const double* src, double* dst, int ni, int nj, int nk, int kfirst, int klast,
-                     double a, double b, cudaStream_t st) {
-    if (a == 0.0) return launch_tb_impl<C, true>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
-    return launch_tb_impl<C, false>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+                     double a, double b, cudaStream_t st, int64_t pitch = 0) {
+    if (a == 0.0)
+        return launch_tb_impl<C, true>(src, dst, ni, nj, nk, kfirst, klast, a, b, st, pitch);
+    return launch_tb_impl<C, false>(src, dst, ni, nj, nk, kfirst, klast, a, b, st, pitch);
 }
 
 // tile configurations per depth: <T, RJ rows/thread, NW warps, S ring stages, MINB,
@@ -375,10 +379,10 @@ static int with_cfg(int T, F&& f) {
 }
 
 static int launch_depth(int T, const double* src, double* dst, int ni, int nj, int nk, int kfirst,
-                        int klast, double a, double b, cudaStream_t st) {
+                        int klast, double a, double b, cudaStream_t st, int64_t pitch = 0) {
     if (klast <= kfirst) return SB_OK;
     return with_cfg(T, [&](auto cfg) {
-        return launch_tb<decltype(cfg)>(src, dst, ni, nj, nk, kfirst, klast, a, b, st);
+        return launch_tb<decltype(cfg)>(src, dst, ni, nj, nk, kfirst, klast, a, b, st, pitch);
     });
 }
 
@@ -470,13 +474,71 @@ constexpr int kMaxFusedDepth = 4;
 
 // Advance `iters` Jacobi sweeps between two device buffers whose halos are
 // already equal.  Returns through *in_b whether the result is in `b_buf`.
+// Grids TMA cannot describe directly (odd ni, or buffers not 16-byte
+// aligned) that are worth it run the fused kernel on pitched copies: rows
+// padded to an even number of doubles (outside the tensor maps' extent, so
+// never touched), copied in with cudaMemcpy2D and the result copied back
+// into a_buf.  Two scratch buffers per device, grown on demand.
+struct JacPitched {
+    double* buf[2] = {nullptr, nullptr};
+    size_t cap = 0;  // doubles per buffer
+};
+static JacPitched g_jac_pitched[64];
+static std::mutex g_jac_pitched_mu;
+
+static int jacobi_run_pitched(double* a_buf, int ni, int nj, int nk, int64_t iters, double a,
+                              double b, int depth, cudaStream_t st) {
+    int dev;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev >= 64) return fail(SB_ERR_CUDA, "device index %d unsupported", dev);
+    std::lock_guard<std::mutex> lk(g_jac_pitched_mu);
+    JacPitched& P = g_jac_pitched[dev];
+    const int64_t nip = ni + 2, pitch = (nip + 1) / 2 * 2, rows = int64_t(nj + 2) * (nk + 2);
+    const size_t need = size_t(pitch) * size_t(rows);
+    if (P.cap < need) {
+        if ((P.buf[0] || P.buf[1]) && (e = cudaStreamSynchronize(st)) != cudaSuccess)
+            return cuda_fail(e, "sync");
+        for (double*& q : P.buf) {
+            if (q) cudaFree(q);
+            q = nullptr;
+        }
+        P.cap = 0;
+        for (double*& q : P.buf)
+            if ((e = cudaMalloc(&q, need * sizeof(double))) != cudaSuccess)
+                return cuda_fail(e, "cudaMalloc(pitched Jacobi grid)");
+        P.cap = need;
+    }
+    for (double* q : P.buf)  // both copies carry the Dirichlet halo
+        if ((e = cudaMemcpy2DAsync(q, pitch * 8, a_buf, nip * 8, nip * 8, rows,
+                                   cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+            return cuda_fail(e, "cudaMemcpy2DAsync(in)");
+    double* src = P.buf[0];
+    double* dst = P.buf[1];
+    for (int64_t left = iters; left > 0;) {
+        const int T = (int)std::min<int64_t>(left, depth);
+        int rc = launch_depth(T, src, dst, ni, nj, nk, 1, nk + 1, a, b, st, pitch);
+        if (rc) return rc;
+        left -= T;
+        std::swap(src, dst);
+    }
+    if ((e = cudaMemcpy2DAsync(a_buf, nip * 8, src, pitch * 8, nip * 8, rows,
+                               cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+        return cuda_fail(e, "cudaMemcpy2DAsync(out)");
+    return SB_OK;
+}
+
 int jacobi_run(double* a_buf, double* b_buf, int ni, int nj, int nk, int64_t iters, double a,
                double b, int depth, cudaStream_t st, int* in_b) {
     const bool tma = tma_ok(a_buf, ni) && tma_ok(b_buf, ni);
+    depth = std::min(depth, kMaxFusedDepth);
+    if (!tma && depth > 1 && int64_t(ni) * nj * nk * iters >= (int64_t(1) << 22)) {
+        *in_b = 0;
+        return jacobi_run_pitched(a_buf, ni, nj, nk, iters, a, b, depth, st);
+    }
     double* src = a_buf;
     double* dst = b_buf;
     int64_t left = iters;
-    depth = std::min(depth, kMaxFusedDepth);
     while (left > 0) {
         int T = (int)((left >= depth) ? depth : left);
         if (!tma) T = 1;

@@ -1,5 +1,6 @@
 // sb_internal.h -- declarations shared by the library's translation units.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <vector>
@@ -12,6 +13,8 @@ void clear_error();
 const char* last_error();
 
 int check_dims(int64_t ni, int64_t nj, int64_t nk);
+int make_grid_map3p(CUtensorMap* m, const double* base, int64_t nip, int64_t njp, int64_t nkp,
+                    int bw, int bh, int bd, int64_t pitch);
 int get_counters(int** counters, int* sms);
 bool tma_ok(const void* p, int64_t ni);
 int halo_copy(const double* src, double* dst, int ni, int nj, int nk, cudaStream_t st);

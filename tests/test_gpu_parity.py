@@ -337,3 +337,16 @@ def test_gs_odd_row_pitch_pitched_path(shape, iters):
         want = oracle.run_serial(kernel, data, iters, 0.0, 1 / 6)
         got = run_device(kernel, data, iters, 0.0, 1 / 6, 1)
         assert sha(got) == sha(want), (shape, kernel)
+
+
+@pytest.mark.parametrize("shape,iters", [((129, 70, 48), 12), ((255, 40, 33), 9)])
+def test_jacobi_odd_row_pitch_pitched_path(shape, iters):
+    """Odd ni: fused depths run on pitched copies -- bitwise equal to the
+    oracle at every depth."""
+    data = make_input({"shape": list(shape), "pattern": "random", "seed": 23, "lo": 0.0,
+                       "hi": 1.0}).data
+    for a, b in ((0.0, 1 / 6), (0.5, 0.1)):
+        want = oracle.run_serial("jacobi", data, iters, a, b)
+        for depth in (1, 2, 3, 4):
+            got = run_device("jacobi", data, iters, a, b, depth)
+            assert sha(got) == sha(want), (shape, a, depth)
