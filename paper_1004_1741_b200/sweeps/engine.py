@@ -44,10 +44,8 @@ def resolve_depth(plan, g):
         depth = plan.config.threads_per_group
     else:
         depth = DEFAULT_DEPTH
-    depth = max(1, min(depth, _lib.max_depth()))
-    if g.ni % 2:  # odd row pitch: no TMA description, single-sweep kernel
-        depth = 1
-    return depth
+    # (odd ni: the library runs the fused depths on pitched copies)
+    return max(1, min(depth, _lib.max_depth()))
 
 
 def _scratch_for(t):

@@ -19,7 +19,7 @@ trials = int(sys.argv[1]) if len(sys.argv) > 1 else 40
 rng = np.random.default_rng(2024)
 bad = 0
 for t in range(trials):
-    ni = int(rng.integers(8, 200)) * 2
+    ni = int(rng.integers(16, 400))  # odd ni: the pitched-copy paths
     nj, nk = (int(x) for x in rng.integers(4, 160, size=2))
     kernel = ("gs-naive", "gs-interleaved", "jacobi")[t % 3]
     iters = int(rng.integers(1, 12))
