@@ -223,12 +223,12 @@ def _device_field(ni, nj, nk, halo=0.0, seed=1):
     return x
 
 
-def _jacobi_dev(x, iters, depth):
+def _jacobi_dev(x, iters, depth, a=0.0, b=1 / 6):
     lib = _lib.load()
     nk, nj, ni = (d - 2 for d in x.shape)
     g, s = x.clone(), torch.empty_like(x)
     in_s = ctypes.c_int(-1)
-    _lib.check(lib.sb_jacobi(g.data_ptr(), s.data_ptr(), ni, nj, nk, iters, 0.0, 1 / 6, depth,
+    _lib.check(lib.sb_jacobi(g.data_ptr(), s.data_ptr(), ni, nj, nk, iters, a, b, depth,
                              None, ctypes.byref(in_s)))
     _lib.check(lib.sb_sync(None))
     out = s if in_s.value else g
@@ -236,14 +236,17 @@ def _jacobi_dev(x, iters, depth):
     return out
 
 
-@pytest.mark.parametrize("shape,iters", [((1024, 1024, 1024), 12), ((1024, 1024, 2048), 4)])
-def test_config4_full_size_depth_independent(shape, iters):
+@pytest.mark.parametrize("shape,iters,coeffs", [((1024, 1024, 1024), 12, (0.0, 1 / 6)),
+                                                ((1024, 1024, 2048), 4, (0.0, 1 / 6)),
+                                                ((1024, 1024, 1024), 8, (0.5, 0.1))])
+def test_config4_full_size_depth_independent(shape, iters, coeffs):
     """Config 4 at full size: depths 2, 3, 4 (the item-list schedule at
-    1024^3) are bitwise equal to depth 1, sweep for sweep."""
+    1024^3) are bitwise equal to depth 1, sweep for sweep (also with a
+    nonzero centre weight: the kernel variant without the a == 0 shortcut)."""
     x = _device_field(*shape)
-    want = _jacobi_dev(x, iters, 1)
+    want = _jacobi_dev(x, iters, 1, *coeffs)
     for depth in (4, 3, 2):
-        got = _jacobi_dev(x, iters, depth)
+        got = _jacobi_dev(x, iters, depth, *coeffs)
         assert torch.equal(got, want), (shape, depth)
         del got
     torch.cuda.empty_cache()
