@@ -353,3 +353,27 @@ def test_jacobi_odd_row_pitch_pitched_path(shape, iters):
         for depth in (1, 2, 3, 4):
             got = run_device("jacobi", data, iters, a, b, depth)
             assert sha(got) == sha(want), (shape, a, depth)
+
+
+@pytest.mark.parametrize("kernel", ["gs-naive", "gs-interleaved"])
+def test_gs_full_size_schedule_independent(kernel):
+    """GS at 1024^3 (beyond the oracle): one call of 6 sweeps (16 x 6 tiles,
+    pipelined sweeps) equals six calls of one sweep (16 x 16 tiles) and three
+    calls of two, bit for bit -- the lexicographic order does not depend on
+    the tile shape, the ticket window or how sweeps are batched."""
+    lib = _lib.load()
+    n = 1024
+    kid = _lib.KERNEL_IDS[kernel]
+    x = _device_field(n, n, n, seed=3) * 2 - 1
+    x[0], x[-1], x[:, 0], x[:, -1], x[:, :, 0], x[:, :, -1] = 0, 0, 0, 0, 0, 0
+    outs = []
+    for split in ((6,), (1,) * 6, (2, 2, 2)):
+        g = x.clone()
+        for it in split:
+            _lib.check(lib.sb_gs(g.data_ptr(), n, n, n, it, 1 / 6, kid, None))
+        _lib.check(lib.sb_sync(None))
+        outs.append(g)
+    del x
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    del outs
+    torch.cuda.empty_cache()
