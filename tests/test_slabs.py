@@ -263,3 +263,38 @@ def test_gs_slab_engine_single_rank_matches_oracle():
     torch.cuda.synchronize()
     want = oracle.run_serial("gs-naive", g.data, 6, 0.0, 1 / 6)
     assert sha(eng.owned().cpu().numpy()) == sha(want[1:-1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nslabs", [2, 8])
+def test_c_abi_gs_slabs_full_size(nslabs):
+    """Config 5's shape (512^3, U[-1,1)): the GS z-pipeline over `nslabs`
+    plane slabs on one GPU == sb_gs on the whole grid, bitwise (4 sweeps)."""
+    import ctypes
+
+    import torch
+
+    from paper_1004_1741_b200 import _lib
+    from paper_1004_1741_b200.slabs import gs_slab_layout
+
+    lib = _lib.load()
+    n, iters = 512, 4
+    x = torch.rand((n + 2, n + 2, n + 2), dtype=torch.float64, device="cuda",
+                   generator=torch.Generator(device="cuda").manual_seed(5)) * 2 - 1
+    x[0], x[-1], x[:, 0], x[:, -1], x[:, :, 0], x[:, :, -1] = 0, 0, 0, 0, 0, 0
+    bufs = []
+    for s in range(nslabs):
+        lo, hi = gs_slab_layout(n, nslabs, s)
+        bufs.append(x[lo - 1:hi + 1].clone())
+    whole = x.clone()
+    _lib.check(lib.sb_gs(whole.data_ptr(), n, n, n, iters, 1 / 6, 1, None))
+    _lib.check(lib.sb_sync(None))
+    st = torch.cuda.Stream()
+    devs = (ctypes.c_int * nslabs)(*([0] * nslabs))
+    pa = (ctypes.c_void_p * nslabs)(*[t.data_ptr() for t in bufs])
+    ps = (ctypes.c_void_p * nslabs)(*([st.cuda_stream] * nslabs))
+    _lib.check(lib.sb_gs_slabs(nslabs, devs, pa, n, n, n, iters, 1 / 6, 1, ps))
+    torch.cuda.synchronize()
+    for s in range(nslabs):
+        lo, hi = gs_slab_layout(n, nslabs, s)
+        assert torch.equal(bufs[s][1:-1], whole[lo:hi]), s
