@@ -409,6 +409,7 @@ def run_gpu_arm(args):
                    "path": "sb_run_host_batch (C ABI; pinned host grids; per step H2D + sweeps "
                            "+ D2H inside the timed region, consecutive steps overlapped)"}
             del host2, host3
+            _lib.release_caches(local)  # the batch's six 8.6 GB device grids
         else:
             e2e = run_e2e_engine(torch, dist, eng, host, args, dev, world)
         del host

@@ -189,6 +189,15 @@ int sb_run_host_batch(int kernel, double* const* host_grids, int count, int64_t 
 int sb_triad(double* a, const double* b, const double* c, double s, int64_t n, void* stream);
 
 /*
+ * Frees the device buffers the library keeps between calls on `device` (all
+ * devices if < 0): the host-entry slots of sb_run_host / sb_run_host_batch
+ * (the batch holds up to six grids' worth) and the pitched copies used for
+ * odd ni.  Synchronises those devices first.  Small per-shape state (work
+ * lists, counters) stays.  The next call reallocates what it needs.
+ */
+int sb_release_caches(int device);
+
+/*
  * Pinned host allocation for grids (so sb_run_host copies at full PCIe
  * rate).  Returns NULL on failure.
  */

@@ -51,6 +51,7 @@ SIGNATURES = {
     "sb_run_host_batch": (_int, [_int, _vp, _int, _i64, _i64, _i64, _i64, _dbl, _dbl, _int, _int]),
     "sb_triad": (_int, [_vp, _vp, _vp, _dbl, _i64, _vp]),
     "sb_host_alloc": (_vp, [_i64]),
+    "sb_release_caches": (_int, [_int]),
     "sb_host_free": (None, [_vp]),
     "sb_jacobi_planes": (_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _int, _dbl, _dbl, _vp]),
     "sb_slab_layout": (_int, [_i64, _int, _int, _int, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
@@ -121,6 +122,12 @@ def require_device():
 
 def max_depth():
     return load().sb_max_depth()
+
+
+def release_caches(device=-1):
+    """Free the device buffers cached between host-entry calls
+    (sb_release_caches)."""
+    check(load().sb_release_caches(device))
 
 
 def jacobi_schedule(sweeps, ni, nj, k_lo, k_hi, ctas):

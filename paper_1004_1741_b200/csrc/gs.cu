@@ -683,6 +683,14 @@ struct GsPitched {
 };
 static GsPitched g_gs_pitched[16];
 
+// frees the pitched-copy buffer of `dev` (caller synchronised the device)
+void gs_release(int dev) {
+    if (dev < 0 || dev >= 16) return;
+    if (g_gs_pitched[dev].buf) cudaFree(g_gs_pitched[dev].buf);
+    g_gs_pitched[dev].buf = nullptr;
+    g_gs_pitched[dev].cap = 0;
+}
+
 static int gs_run_pitched(double* grid, int ni, int nj, int nk, int64_t iters, double b,
                           bool inter, cudaStream_t st) {
     int dev;

@@ -143,6 +143,30 @@ static void batch_free(BatchCtx& B) {
     B.cap = 0;
 }
 
+int sb_release_caches(int device) {
+    clear_error();
+    const int ndev = sb_device_count();
+    int cur = 0;
+    if (ndev > 0 && cudaGetDevice(&cur) != cudaSuccess) return fail(SB_ERR_CUDA, "cudaGetDevice");
+    for (int d = 0; d < std::min(ndev, 64); ++d) {
+        if (device >= 0 && d != device) continue;
+        cudaError_t e = cudaSetDevice(d);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return cuda_fail(e, "sb_release_caches");
+        std::lock_guard<std::mutex> lk(g_host_mu);
+        batch_free(g_batch[d]);
+        HostCtx& H = g_host[d];
+        if (H.g) cudaFree(H.g);
+        if (H.s) cudaFree(H.s);
+        H.g = H.s = nullptr;
+        H.cap = 0;
+        gs_release(d);
+        jacobi_release(d);
+    }
+    if (ndev > 0) cudaSetDevice(cur);
+    return SB_OK;
+}
+
 int sb_run_host_batch(int kernel, double* const* host_grids, int count, int64_t ni, int64_t nj,
                       int64_t nk, int64_t iters, double a, double b, int depth, int device) {
     clear_error();

@@ -486,6 +486,17 @@ struct JacPitched {
 static JacPitched g_jac_pitched[64];
 static std::mutex g_jac_pitched_mu;
 
+// frees the pitched-copy buffers of `dev` (caller synchronised the device)
+void jacobi_release(int dev) {
+    if (dev < 0 || dev >= 64) return;
+    std::lock_guard<std::mutex> lk(g_jac_pitched_mu);
+    for (double*& q : g_jac_pitched[dev].buf) {
+        if (q) cudaFree(q);
+        q = nullptr;
+    }
+    g_jac_pitched[dev].cap = 0;
+}
+
 static int jacobi_run_pitched(double* a_buf, int ni, int nj, int nk, int64_t iters, double a,
                               double b, int depth, cudaStream_t st) {
     int dev;

@@ -33,4 +33,7 @@ std::vector<int4> build_item_list(int T, int tiles_i, int tiles_j, const std::ve
 int item_list(int T, int tiles_i, int tiles_j, const std::vector<char>& border, int kfirst,
               int klast, int grid, int kb, const int4** out, int* count);
 
+void gs_release(int dev);
+void jacobi_release(int dev);
+
 }  // namespace sb

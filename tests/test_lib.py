@@ -132,3 +132,9 @@ def test_schedule_rejects_bad_arguments():
     assert lib.sb_jacobi_schedule(4, 64, 64, 1, 9, 0, None, 0, ctypes.byref(n), None) != 0
     assert lib.sb_jacobi_schedule(4, 64, 64, 1, 9, 148, None, 0, ctypes.byref(n), None) == 0
     assert n.value > 0
+
+
+def test_release_caches_without_device_is_a_no_op():
+    lib = _lib.load()
+    if _lib.device_count() == 0:
+        assert lib.sb_release_caches(-1) == 0
