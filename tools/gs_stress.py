@@ -16,7 +16,7 @@ from paper_1004_1741_b200 import InitPattern, create_grid  # noqa: E402
 from paper_1004_1741_b200.sweeps import execute  # noqa: E402
 
 trials = int(sys.argv[1]) if len(sys.argv) > 1 else 40
-rng = np.random.default_rng(2024)
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2024)
 bad = 0
 for t in range(trials):
     ni = int(rng.integers(16, 400))  # odd ni: the pitched-copy paths
