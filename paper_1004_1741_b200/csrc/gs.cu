@@ -554,7 +554,7 @@ static std::vector<int2> wavefront_order(int tiles_j, int tiles_k, int sweeps, i
 }
 
 static int gs_window() {
-    static int w = getenv("SB_GS_WINDOW") ? std::max(1, atoi(getenv("SB_GS_WINDOW"))) : 3;
+    static int w = tune_env("SB_GS_WINDOW") ? std::max(1, atoi(tune_env("SB_GS_WINDOW"))) : 3;
     return w;
 }
 
@@ -611,17 +611,12 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
     if ((rc = make_grid_map3p(&lmap, grid, nip, njp, nkp, C::CW, C::LJ, C::LK, pitch))) return rc;
     if ((rc = make_grid_map3p(&smap, grid, nip, njp, nkp, C::CW, C::BJ, 1, pitch))) return rc;
 
-    static int occ = -1;
     auto kern_n = gs_tile_kernel<C, false>;
     auto kern_i = gs_tile_kernel<C, true>;
-    if (occ < 0) {
-        for (auto k : {kern_n, kern_i}) {
-            e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(gs)");
-        }
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern_n, C::NT, C::SMEM_BYTES);
-        if (e != cudaSuccess || occ < 1) return fail(SB_ERR_CUDA, "gs kernel does not fit");
-    }
+    int occ = 0;
+    if ((rc = ctas_per_sm((const void*)kern_i, C::NT, C::SMEM_BYTES, &occ)) ||
+        (rc = ctas_per_sm((const void*)kern_n, C::NT, C::SMEM_BYTES, &occ)))
+        return rc;
     GsParams p;
     p.ni = ni;
     p.nj = nj;
@@ -733,7 +728,7 @@ int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int ke
         return gs_run_pitched(grid, ni, nj, nk, iters, b,
                               kernel == SB_KERNEL_GS_INTERLEAVED && ni >= 2, st);
     }
-    static const int v = getenv("SB_GSCFG") ? atoi(getenv("SB_GSCFG")) : 0;  // tuning
+    static const int v = tune_env("SB_GSCFG") ? atoi(tune_env("SB_GSCFG")) : 0;  // tuning
     const bool inter = kernel == SB_KERNEL_GS_INTERLEAVED;
     // one or two sweeps per call (the GS z-pipeline's stages): the 16 x 16
     // tiles' shorter tile-wavefront fill wins (512^3: 1 sweep 0.90 vs 1.31 ms,

@@ -68,9 +68,16 @@ struct JacobiParams {
     int64_t plane;           // (nj + 2) * (ni + 2) cells, < 2^31 (check_dims)
 };
 
-template <int T_, int RJ_, int NW_, int S_, int MINB_, bool L1S_ = false, bool TS_ = false>
+template <int T_, int RJ_, int NW_, int S_, int MINB_, bool L1S_ = false, bool TS_ = false,
+          bool UNI_ = false>
 struct JacobiCfg {
     static constexpr int T = T_, RJ = RJ_, NW = NW_, S = S_, MINB = MINB_;
+    // UNI: one step loop for every step of an item (StepMode MASK: the FAST
+    // arithmetic, then a per-cell select against Dirichlet masks that also
+    // cover the k-boundary planes) instead of SLOW / FAST|SEL / SLOW loops.
+    // One inlined loop instead of three leaves ptxas room for 5 rows per
+    // thread at T = 4 without spilling.
+    static constexpr bool UNI = UNI_;
     // TS: level T writes its output tile into a shared staging buffer (double
     // buffered) and one thread stores it with a TMA tensor store per plane,
     // instead of per-thread 16-byte global stores
@@ -256,8 +263,13 @@ __device__ __forceinline__ void produce(const CUtensorMap* src_map, const Jacobi
 // SEL: the planes are interior but the tile touches the i/j boundary: the
 // FAST arithmetic, then Dirichlet cells keep their value (per-item masks).
 // SLOW: anything (k-boundary steps, tiny grids): full predication, and rows
-// outside a level's trapezoid skip their arithmetic.
-enum StepMode { SLOW = 0, FAST = 1, SEL = 2 };
+// outside a level's trapezoid skip their arithmetic.  MASK (JacobiCfg::UNI):
+// any step, FAST arithmetic everywhere, then Dirichlet cells -- i/j masks
+// of the item, plus every cell of a level whose plane lies outside [1, nk] --
+// keep their value.  Cells outside a level's trapezoid then hold values that
+// no output depends on (level L+1 reads level L only inside its own,
+// smaller, trapezoid grown by one cell).
+enum StepMode { SLOW = 0, FAST = 1, SEL = 2, MASK = 3 };
 
 // One level's update of a thread's RJ rows x 2 cells in one pass (SEL and
 // SLOW steps).  cen: the centre
@@ -354,6 +366,10 @@ __device__ __forceinline__ void level_finish(const double (&cc)[C::RJ][2],
         } else if (MODE == SEL) {
             nv[r][0] = (s.keep0 & (1u << r)) ? c0 : o0;
             nv[r][1] = (s.keep1 & (1u << r)) ? c1 : o1;
+        } else if (MODE == MASK) {
+            const uint32_t kall = (k < 1 || k > p.nk) ? 0xffffffffu : 0u;  // CTA-uniform
+            nv[r][0] = ((s.keep0 | kall) & (1u << r)) ? c0 : o0;
+            nv[r][1] = ((s.keep1 | kall) & (1u << r)) ? c1 : o1;
         } else {
             const int jr = dj + r, need = T - L;
             const bool compute = (jr >= -need) && (jr < C::TJ + need) && (k >= 1) &&
@@ -460,7 +476,7 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
         cen[RJ + 1][1] = n2.y;
     };
 
-    if constexpr (MODE == FAST) {
+    if constexpr (MODE == FAST || MODE == MASK) {
         // ---- phase 1: partial sums of every level (previous-step data) ----
         double P1[RJ][2], C1[RJ][2];  // L1S: level 1's P and centre plane (else unused)
 #pragma unroll
@@ -684,12 +700,19 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
                            (jlo >= 1) && (jlo + C::ROWS - 1 <= p.nj);
         const int n_lo = min(s.it.N, max(0, 2 * T + 1 - s.it.kb));
         const int n_hi = max(n_lo, min(s.it.N, p.nk + 2 + T - s.it.kb));
-        jacobi_steps<C, SLOW, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, n_lo);
-        if (ij_in)
-            jacobi_steps<C, FAST, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, n_hi - n_lo);
-        else
-            jacobi_steps<C, SEL, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, n_hi - n_lo);
-        jacobi_steps<C, SLOW, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, s.it.N - n_hi);
+        if constexpr (C::UNI) {
+            jacobi_steps<C, MASK, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, s.it.N);
+        } else {
+            jacobi_steps<C, SLOW, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, n_lo);
+            if (ij_in)
+                jacobi_steps<C, FAST, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
+                                          n_hi - n_lo);
+            else
+                jacobi_steps<C, SEL, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
+                                         n_hi - n_lo);
+            jacobi_steps<C, SLOW, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
+                                      s.it.N - n_hi);
+        }
         s.n = 0;
         __syncthreads();  // queue[] entry written by thread 0 at least one barrier ago
         s.cq = (s.cq + 1) % C::QSLOTS;

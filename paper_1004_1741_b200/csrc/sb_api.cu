@@ -127,6 +127,30 @@ int dev_ctx(DevCtx** out) {
     return SB_OK;
 }
 
+int ctas_per_sm(const void* kern, int threads, size_t smem, int* out) {
+    int dev;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> known;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = known.find({kern, dev});
+    if (it != known.end()) {
+        *out = it->second;
+        return SB_OK;
+    }
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+        return cuda_fail(e, "cudaFuncSetAttribute");
+    int o = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem)) != cudaSuccess)
+        return cuda_fail(e, "occupancy query");
+    if (o < 1) return fail(SB_ERR_CUDA, "kernel does not fit on an SM (%zu B shared memory)", smem);
+    known[{kern, dev}] = o;
+    *out = o;
+    return SB_OK;
+}
+
 int get_counters(int** counters, int* sms) {
     DevCtx* c;
     int rc = dev_ctx(&c);
@@ -241,7 +265,7 @@ static TbPlan tb_plan(int ni, int nj, int kfirst, int klast, int grid) {
     pl.tiles_j = (nj + C::TJ - 1) / C::TJ;
     const int nkout = klast - kfirst;
     int kb = pick_kblock(C::T, pl.tiles_i * pl.tiles_j, nkout, grid);
-    static const int kb_env = getenv("SB_KBLK") ? atoi(getenv("SB_KBLK")) : 0;  // tuning
+    static const int kb_env = tune_env("SB_KBLK") ? atoi(tune_env("SB_KBLK")) : 0;  // tuning
     if (kb_env > 0) kb = kb_env;
     pl.kb = std::max(1, std::min(kb, nkout));
     pl.list_ok = kb_env <= 0;
@@ -255,19 +279,10 @@ static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk
     int sms;
     int rc = get_counters(&counters, &sms);
     if (rc) return rc;
-    static int occ = -1;  // per instantiation (one device type per process)
     auto kern = jacobi_tb_kernel<C, AZ>;
-    if (occ < 0) {
-        cudaError_t e =
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-        int o = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::NT, C::SMEM_BYTES);
-        if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
-        o *= sms;  // CTAs on the device
-        if (o < 1) return fail(SB_ERR_CUDA, "jacobi T=%d kernel does not fit on an SM", C::T);
-        occ = o;
-    }
+    int per_sm = 0;
+    if ((rc = ctas_per_sm((const void*)kern, C::NT, C::SMEM_BYTES, &per_sm))) return rc;
+    const int occ = per_sm * sms;  // resident CTAs on the device
     CUtensorMap smap, dmap;
     const int64_t nip = ni + 2, njp = nj + 2, nkp = nk + 2;
     if (pitch <= 0) pitch = nip;
@@ -330,45 +345,42 @@ static int launch_tb(const double* src, double* dst, int ni, int nj, int nk, int
     return launch_tb_impl<C, false>(src, dst, ni, nj, nk, kfirst, klast, a, b, st, pitch);
 }
 
-// tile configurations per depth: <T, RJ rows/thread, NW warps, S ring stages, MINB,
-// L1S level 1 from the ring, TS TMA-store output>
-// (SB_JCFG=<variant> selects alternatives during tuning)
+// Tile configurations per depth: <T, RJ rows/thread, NW warps, S ring stages,
+// MINB, L1S level 1 from the ring, TS TMA-store output>.
+// Builds with -DSB_EXPERIMENTS (tools/, never the product library) also carry
+// the alternatives measured while tuning, selected with SB_JCFG=<variant>.
+#ifdef SB_EXPERIMENTS
 static int jcfg_variant() {
     static int v = getenv("SB_JCFG") ? atoi(getenv("SB_JCFG")) : 0;
     return v;
 }
+#endif
 
 // Calls f(JacobiCfg<...>{}) with the tile configuration of depth T.
 template <class F>
 static int with_cfg(int T, F&& f) {
-    const int v = jcfg_variant();
 #define SB_L(...) return f(JacobiCfg<__VA_ARGS__>{})
+#ifdef SB_EXPERIMENTS
+    const int v = jcfg_variant();
     switch (T) {
-        case 1:
-            if (v == 1) SB_L(1, 2, 8, 4, 4);
-            if (v == 4) SB_L(1, 4, 8, 4, 2);
-            SB_L(1, 4, 8, 4, 2, false, true);
-        case 2:
-            if (v == 1) SB_L(2, 4, 8, 4, 2);
-            if (v == 2) SB_L(2, 4, 12, 5, 1, true);
-            if (v == 5) SB_L(2, 4, 8, 4, 2, true);
-            SB_L(2, 4, 8, 8, 1, false, true);
         case 3:
-            if (v == 1) SB_L(3, 2, 16, 4, 1);
-            if (v == 2) SB_L(3, 3, 16, 5, 1, true);
-            if (v == 3) SB_L(3, 4, 8, 4, 2, true);
-            if (v == 4) SB_L(3, 4, 12, 5, 1, true);
-            if (v == 5) SB_L(3, 4, 12, 5, 1, true, true);
-            if (v == 6) SB_L(3, 4, 8, 9, 1, false, true);
-            SB_L(3, 4, 8, 8, 1, false, true);
+            if (v == 7) SB_L(3, 5, 8, 6, 1, false, true);
+            if (v == 10) SB_L(3, 4, 8, 8, 1, false, true, true);
+            if (v == 11) SB_L(3, 5, 8, 6, 1, false, true, true);
+            if (v == 12) SB_L(3, 6, 8, 5, 1, false, true, true);
+            break;
         case 4:
-            if (v == 1) SB_L(4, 2, 16, 4, 1);
-            if (v == 2) SB_L(4, 4, 12, 5, 1, true);
-            if (v == 3) SB_L(4, 3, 16, 5, 1, true);
-            if (v == 4) SB_L(4, 4, 8, 4, 1);
-            if (v == 5) SB_L(4, 4, 8, 4, 1, false, true);
-            if (v == 6) SB_L(4, 4, 8, 9, 1, false, true);
-            SB_L(4, 4, 8, 8, 1, false, true);
+            if (v == 10) SB_L(4, 4, 8, 8, 1, false, true, true);
+            if (v == 11) SB_L(4, 5, 8, 6, 1, false, true, true);
+            if (v == 12) SB_L(4, 5, 8, 5, 1, false, true, true);
+            break;
+    }
+#endif
+    switch (T) {
+        case 1: SB_L(1, 4, 8, 4, 2, false, true);
+        case 2: SB_L(2, 4, 8, 8, 1, false, true);
+        case 3: SB_L(3, 4, 8, 8, 1, false, true);
+        case 4: SB_L(4, 4, 8, 8, 1, false, true);
         case 5: SB_L(5, 2, 12, 3, 1);
         case 6: SB_L(6, 2, 12, 3, 1);
         case 7: SB_L(7, 2, 12, 3, 1);

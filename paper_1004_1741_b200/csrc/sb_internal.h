@@ -3,11 +3,30 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 
 namespace sb {
 
+// Tuning knobs (SB_KBLK, SB_LIST*, SB_GS_WINDOW, SB_GSCFG, SB_JCFG) are read
+// from the environment only in experiment builds (-DSB_EXPERIMENTS, tools/);
+// the product library always runs its measured defaults.
+inline const char* tune_env(const char* name) {
+#ifdef SB_EXPERIMENTS
+    return getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
+
 int fail(int code, const char* fmt, ...);
+
+// Resident CTAs per SM of `kern` on the current device, with its dynamic
+// shared-memory opt-in made first.  The opt-in is a property of each
+// device's context, so it is made once per (kernel, device) -- not once per
+// process (sb_api.cu).
+int ctas_per_sm(const void* kern, int threads, size_t smem, int* out);
 int cuda_fail(cudaError_t e, const char* what);
 void clear_error();
 const char* last_error();

@@ -35,12 +35,12 @@ struct Item {
 };
 
 double env_double(const char* name, double dflt) {
-    const char* v = getenv(name);
+    const char* v = tune_env(name);
     return v ? atof(v) : dflt;
 }
 
 int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
+    const char* v = tune_env(name);
     return v ? atoi(v) : dflt;
 }
 
@@ -197,7 +197,7 @@ std::vector<int4> build_item_list(int T, int tiles_i, int tiles_j, const std::ve
         else
             for (int nb = 1; nb <= 32; ++nb) params.push_back((nk + nb - 1) / nb);
     }
-    const bool force = getenv("SB_LIST_FORCE") != nullptr;
+    const bool force = tune_env("SB_LIST_FORCE") != nullptr;
     for (int prm : params) {
         std::vector<Item> v = build_list(mode, T, tiles_i, tiles_j, border, kfirst, klast, grid, prm);
         if (v.empty()) continue;

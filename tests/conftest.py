@@ -40,9 +40,34 @@ def coeffs_of(rec):
 
 
 def sha(a):
+    """sha256 of the C-order little-endian float64 bytes (hashed plane by
+    plane: no copy of a multi-GB grid)."""
     import hashlib
 
-    return hashlib.sha256(np.ascontiguousarray(a, dtype="<f8").tobytes()).hexdigest()
+    a = np.ascontiguousarray(a, dtype="<f8")
+    h = hashlib.sha256()
+    for plane in a.reshape(a.shape[0], -1) if a.ndim > 1 else [a]:
+        h.update(memoryview(plane))
+    return h.hexdigest()
+
+
+def sha_device(t, chunk_planes=64):
+    """sha() of a CUDA float64 tensor, downloaded a few planes at a time."""
+    import hashlib
+
+    import torch
+
+    h = hashlib.sha256()
+    buf = None
+    for k0 in range(0, t.shape[0], chunk_planes):
+        part = t[k0:k0 + chunk_planes]
+        if buf is None or buf.shape != part.shape:
+            buf = torch.empty(part.shape, dtype=t.dtype, pin_memory=True)
+        buf.copy_(part)
+        a = buf.numpy()
+        for plane in a.reshape(a.shape[0], -1):
+            h.update(memoryview(plane))
+    return h.hexdigest()
 
 
 @pytest.fixture(scope="session")

@@ -51,7 +51,13 @@ GC = (0.0, 1.0 / 6.0)      # reference default / GS coefficients
 
 
 def sha(a):
-    return hashlib.sha256(np.ascontiguousarray(a, dtype="<f8").tobytes()).hexdigest()
+    """sha256 of the C-order little-endian float64 bytes, hashed plane by
+    plane so a 17 GB grid is never duplicated in host memory."""
+    a = np.ascontiguousarray(a, dtype="<f8")
+    h = hashlib.sha256()
+    for plane in a.reshape(a.shape[0], -1):
+        h.update(memoryview(plane))
+    return h.hexdigest()
 
 
 def make_input(spec):
@@ -84,7 +90,8 @@ def ref_result(kernel, sp, iters, coeffs, variant="serial", **kw):
     in_hash = sha(g.data)
     plan = SweepPlan(kernel, variant, iters, coeffs=StencilCoeffs(*coeffs), **kw)
     out = run_serial(plan, g) if variant == "serial" else run(plan, g)
-    return in_hash, np.array(out.data, copy=True)
+    # the engines return a grid the caller owns (g or the scratch copy)
+    return in_hash, out.data
 
 
 SMALL = [
@@ -142,6 +149,15 @@ HASHED = [
     ("aniso_gsn", "gs-naive", spec((250, 34, 18)), [3], GC),
 ]
 
+# BASELINE config 4 (the bench's headline): weak-scaling 1024^3 per GPU and the
+# strong-scaling 1024 x 1024 x 2048 grid, 100 sweeps.  ``--huge``: ~5 + ~10
+# minutes on 8 cores with the reference's threaded k-slab engine; the 2048
+# case peaks at ~52 GB of host memory (grid, uniform temp / scratch copy).
+HUGE = [
+    ("cfg4_jacobi1024", "jacobi", spec((1024, 1024, 1024)), [100], GC),
+    ("cfg4_jacobi1024x2048", "jacobi", spec((1024, 1024, 2048)), [100], GC),
+]
+
 BIG = [
     ("cfg3_jacobi512_halo1", "jacobi", spec((512, 512, 512), halo=1.0), [4, 100], GC),
     ("cfg5_gsn512_mixed", "gs-naive", spec((512, 512, 512), lo=-1.0, hi=1.0), [100], GC),
@@ -181,9 +197,19 @@ def hashed_records(items, threads):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
+    ap.add_argument("--huge", action="store_true",
+                    help="only the config-4 records (skips the small cases)")
     ap.add_argument("--threads", type=int, default=os.cpu_count())
     args = ap.parse_args()
     assert HAVE_NUMBA, "generate with the reference's compiled kernels"
+    hpath = HERE / "hashes.json"
+    if args.huge:
+        hashes = json.loads(hpath.read_text())
+        for name, kernel, sp, iters, coeffs in HUGE:
+            hashes.update(hashed_records([(name, kernel, sp, iters, coeffs)], args.threads))
+            hpath.write_text(json.dumps(hashes, indent=1, sort_keys=True))
+        print(f"wrote {len(hashes)} hashed cases")
+        return
 
     arrays, meta = {}, {}
     for name, kernel, sp, iters, coeffs in SMALL:
@@ -199,7 +225,6 @@ def main():
     (HERE / "small_cases.json").write_text(json.dumps(meta, indent=1, sort_keys=True))
     print(f"wrote {len(arrays)} small cases")
 
-    hpath = HERE / "hashes.json"
     hashes = json.loads(hpath.read_text()) if hpath.exists() else {}
     hashes.update(hashed_records(HASHED, args.threads))
     if args.big:

@@ -19,6 +19,10 @@ def main(rep, top=20):
         for k in keys:
             if k in hdr:
                 print(f"{k} = {r[hdr.index(k)]}")
+        pipes = [(h, r[i]) for i, h in enumerate(hdr)
+                 if ("pipe" in h or "mio" in h or "lsu" in h) and h.endswith("pct_of_peak_sustained_active")]
+        pipes = sorted(((h, float(v)) for h, v in pipes if v not in ("", "n/a")), key=lambda x: -x[1])
+        print("pipes:", ", ".join(f"{h.replace('.avg.pct_of_peak_sustained_active','')}={v:.1f}" for h, v in pipes[:14]))
         st = [(h, r[i]) for i, h in enumerate(hdr) if "smsp__average_warps_issue_stalled" in h and "not_issued" not in h]
         st = sorted(st, key=lambda x: -float(x[1] or 0))
         print("stalls:", ", ".join(f"{h.replace('smsp__average_warps_issue_stalled_','').replace('_per_issue_active.ratio','')}={float(v):.2f}" for h, v in st[:8]))
