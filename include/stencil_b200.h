@@ -122,7 +122,8 @@ int sb_jacobi(double* grid, double* scratch, int64_t ni, int64_t nj, int64_t nk,
  * kernel: SB_KERNEL_GS_NAIVE or SB_KERNEL_GS_INTERLEAVED (selects the
  * association, bitwise equal to the matching reference kernel).
  * Asynchronous on `stream`.  GS calls on one device share its scheduling
- * state: issue them on one stream (or synchronise between streams).
+ * state; calls on different streams of one device are serialised by the
+ * library (each launch waits for the previous one on that device).
  */
 int sb_gs(double* grid, int64_t ni, int64_t nj, int64_t nk, int64_t iters, double b,
           int kernel, void* stream);
@@ -130,10 +131,23 @@ int sb_gs(double* grid, int64_t ni, int64_t nj, int64_t nk, int64_t iters, doubl
 /*
  * Wait for all work queued on `stream` and report deferred failures: a
  * CUDA error raised by the kernels, or SB_ERR_TIMEOUT when a Gauss-Seidel
- * inter-CTA dependency wait expired (the kernel then bails out instead of
- * hanging and the grid content is unspecified).
+ * inter-CTA dependency wait expired.  A timed-out launch is abandoned
+ * cooperatively: every warp of every CTA sees the error word and exits, so
+ * the CUDA context stays usable (the next call runs normally); the grid
+ * content is then unspecified.  This replaces the reference's poisoned
+ * barriers (sync.py:31-32) and worker re-raise (sweeps/team.py:42-64).
  */
 int sb_sync(void* stream);
+
+/*
+ * Test hook (fault injection, used by tests/test_gpu_faults.py): kind 1
+ * makes later Gauss-Seidel launches withhold one progress publish (tile 0,
+ * sweep 0, chunks after the first), so its dependants wait until the
+ * timeout; kind 0 restores normal operation.  timeout_cycles (> 0) sets the
+ * no-progress limit of the inter-CTA waits in SM clock cycles; <= 0 restores
+ * the default 2^35 (~17 s).  Process-wide; affects launches issued later.
+ */
+int sb_debug_fault(int kind, int64_t timeout_cycles);
 
 /*
  * The library's plain "serial engine": straightforward kernels without

@@ -44,6 +44,7 @@ SIGNATURES = {
                          ctypes.POINTER(_int)]),
     "sb_gs": (_int, [_vp, _i64, _i64, _i64, _i64, _dbl, _int, _vp]),
     "sb_sync": (_int, [_vp]),
+    "sb_debug_fault": (_int, [_int, _i64]),
     "sb_line_update": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _dbl, _dbl, _vp]),
     "sb_reference_sweeps": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _dbl, _dbl, _vp,
                                    ctypes.POINTER(_int)]),

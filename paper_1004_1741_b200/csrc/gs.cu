@@ -42,6 +42,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <type_traits>
 #include <utility>
 #include <cstdint>
@@ -64,7 +65,9 @@ struct GsParams {
     double b;
     int* ticket;           // atomic task counter
     int* prog;             // [R][ntiles] progress (encoded)
-    int* err;              // error word (timeout)
+    int* err;              // error word (timeout): every role polls it and exits
+    long long timeout;     // cycles without progress before a wait gives up
+    int fault;             // test-only fault injection (sb_debug_fault), 0 = none
     const int2* order;     // ticket -> (sweep, J | K << 16), in wavefront order
     double* grid;          // the grid
     unsigned long long* prof;  // SB_GS_PROFILE builds: per-CTA cycle counters
@@ -90,7 +93,7 @@ struct GsCfg {
     // line's chunk (the rest of the ring is prefetch)
     static_assert((NS - 2) * CW >= SMAX + 3, "too few chunk slots for the skew");
     static constexpr size_t SMEM_BYTES = size_t(NS) * SLOT * 8 + 24 * NS + 16 * QS + 64;
-    // (full[NS], empty[NS], one spare barrier row, task queue)
+    // (full[NS], done[NS], empty[NS], task queue[QS], abort flag + spare)
 };
 
 struct GsTask {
@@ -163,14 +166,40 @@ __device__ __forceinline__ GsTask decode_task(const GsParams& p, long long tk) {
     return t;
 }
 
-__device__ __forceinline__ void gs_check_abort(const GsParams& p, long long& t0) {
-    if (*reinterpret_cast<volatile int*>(p.err)) __trap();
-    if (clock64() - t0 > (1LL << 35)) {  // ~17 s without progress: never hang
+// Called in every polling loop.  Returns true when the launch is being
+// abandoned: another thread flagged the error word, or this wait went
+// p.timeout cycles without progress (it then flags it).  Every role then
+// leaves its loops and the kernel exits normally, so the CUDA context stays
+// usable and the host reads SB_ERR_TIMEOUT from the error word -- the GPU
+// form of the reference's poisoned barriers (sync.py:31-32, team.py:42-64).
+__device__ __forceinline__ bool gs_abort(const GsParams& p, long long t0) {
+    if (*reinterpret_cast<volatile int*>(p.err)) return true;
+    if (clock64() - t0 > p.timeout) {
         atomicExch(p.err, 1);
         __threadfence();
-        __trap();
+        return true;
     }
     __nanosleep(64);
+    return false;
+}
+
+// A compute-side chunk wait: false when the launch is being abandoned.
+__device__ __forceinline__ bool gs_wait(const GsParams& p, uint64_t* bar, uint32_t parity) {
+    if (mbar_try_wait(bar, parity)) return true;
+    const long long t0 = clock64();
+    while (!mbar_try_wait(bar, parity))
+        if (gs_abort(p, t0)) return false;
+    return true;
+}
+
+// On abort the loader waits for its chunk loads still in flight (each is the
+// latest load of its ring slot) to land before the CTA may exit.
+template <class C>
+__device__ void gs_loader_drain(uint64_t* full, uint32_t gload) {
+    const uint32_t first = gload > uint32_t(C::NS) ? gload - C::NS : 0;
+    for (uint32_t n = first; n < gload; ++n)
+        while (!mbar_try_wait(&full[n % C::NS], (n / C::NS) & 1)) {
+        }
 }
 
 // ---------------------------------------------------------------------------
@@ -200,7 +229,9 @@ __device__ void gs_loader(const CUtensorMap* ld_map, const GsParams& p, double* 
 #endif
             // release the compute warps waiting for this (stop) task's first
             // chunk: complete that slot's barrier phase without data
-            if (gload >= NS) mbar_wait(&empty[slot0], ((gload - NS) / NS) & 1);
+            if (gload >= NS)
+                while (!mbar_try_wait(&empty[slot0], ((gload - NS) / NS) & 1))
+                    if (gs_abort(p, t0)) return gs_loader_drain<C>(full, gload);
             mbar_arrive(&full[slot0]);
             return;
         }
@@ -212,14 +243,15 @@ __device__ void gs_loader(const CUtensorMap* ld_map, const GsParams& p, double* 
             long long ta = clock64();
 #endif
             if (gload >= NS) {  // the slot's previous chunk must have been stored
-                while (!mbar_try_wait(&empty[slot], ((gload - NS) / NS) & 1)) gs_check_abort(p, t0);
+                while (!mbar_try_wait(&empty[slot], ((gload - NS) / NS) & 1))
+                    if (gs_abort(p, t0)) return gs_loader_drain<C>(full, gload);
             }
 #ifdef SB_GS_PROFILE
             long long tb = clock64();
             l_empty += tb - ta;
 #endif
             while (!((c > 0 || prog_ready<C>(p, lt.s - (C::R - 1), lt.tile, nch)) && deps_ready(deps, c)))
-                gs_check_abort(p, t0);
+                if (gs_abort(p, t0)) return gs_loader_drain<C>(full, gload);
 #ifdef SB_GS_PROFILE
             l_deps += clock64() - tb;
 #endif
@@ -246,7 +278,8 @@ __device__ void gs_storer(const CUtensorMap* st_map, const GsParams& p, double* 
     while (true) {
         // the task's first chunk being loaded implies its queue entry is written
         const uint32_t slot0 = gstore % NS;
-        while (!mbar_try_wait(&full[slot0], (gstore / NS) & 1)) gs_check_abort(p, t0);
+        while (!mbar_try_wait(&full[slot0], (gstore / NS) & 1))
+            if (gs_abort(p, t0)) return;
         const GsTask t = queue[sq];
         sq = (sq + 1) % C::QS;
         if (t.s < 0) return;
@@ -254,7 +287,8 @@ __device__ void gs_storer(const CUtensorMap* st_map, const GsParams& p, double* 
         int* flag = p.prog + (t.s % C::R) * p.ntiles + t.tile;
         for (int c = 0; c < nch; ++c, ++gstore) {
             const uint32_t slot = gstore % NS;
-            while (!mbar_try_wait(&done[slot], (gstore / NS) & 1)) gs_check_abort(p, t0);
+            while (!mbar_try_wait(&done[slot], (gstore / NS) & 1))
+                if (gs_abort(p, t0)) return;
             t0 = clock64();
             const double* base = ring + size_t(slot) * C::SLOT;
             for (int q = 0; q < C::BK; ++q)
@@ -264,6 +298,9 @@ __device__ void gs_storer(const CUtensorMap* st_map, const GsParams& p, double* 
             mbar_arrive(&empty[slot]);
             bulk_wait<0>();       // ... and landed in global memory
             fence_proxy_async_global();
+            // test-only fault (sb_debug_fault(1)): tile 0 never publishes
+            // sweep 0 past its first chunk, so its dependants time out
+            if (p.fault == 1 && t.s == 0 && t.tile == 0 && c >= 1) continue;
             st_release(flag, prog_val(t.s, c + 1, nch));
         }
     }
@@ -353,6 +390,7 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
             mbar_init(&done[s], 1);
             mbar_init(&empty[s], 1);
         }
+        *reinterpret_cast<volatile int*>(queue + C::QS) = 0;
         fence_mbar_init();
     }
     __syncthreads();
@@ -374,6 +412,9 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
     // chunk, every thread fences its shared-memory writes for the async proxy
     // and after the barrier thread 0 hands the chunk to the storer.
     constexpr int LPT = C::LPT, KSTEP = C::BK / C::LPT;
+    // abort flag: thread 0 sets it when a chunk wait gives up (gs_abort); the
+    // other compute threads read it after the step barrier that follows
+    volatile int* abort_s = reinterpret_cast<volatile int*>(queue + C::QS);
     const int jl = tid % BJ, kl0 = tid / BJ;
     const double b = p.b;
     const int nch = p.nch, ni = p.ni;
@@ -388,12 +429,14 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
 #ifdef SB_GS_PROFILE
         long long tw = clock64();
 #endif
-        if (tid == 0) mbar_wait(&full[gc % NS], (gc / NS) & 1);  // chunk 0 (+ queue entry)
+        if (tid == 0 && !gs_wait(p, &full[gc % NS], (gc / NS) & 1))  // chunk 0 (+ queue entry)
+            *abort_s = 1;
 #ifdef SB_GS_PROFILE
         w_start += clock64() - tw;
         ++n_tasks;
 #endif
         named_bar_sync(1, C::NCOMP);
+        if (*abort_s) break;
         const GsTask t = queue[q];
         q = (q + 1) % C::QS;
         if (t.s < 0) break;
@@ -411,7 +454,8 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
         constexpr int POS_FIN = ((SMAX - 2) % CW + CW) % CW;    // (st+2-SMAX) % CW == 0
         // One block of CW plane steps.  FULL: every line computes at every step
         // of the block (no prologue/epilogue of the skew, no partial tile).
-        auto block = [&](const int st0, auto full_tag) {
+        // Returns true when the launch is being abandoned (gs_abort).
+        auto block = [&](const int st0, auto full_tag) -> bool {
             constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
             for (int pos = 0; pos < CW; ++pos) {
@@ -435,7 +479,8 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
 #ifdef SB_GS_PROFILE
                         long long tc = clock64();
 #endif
-                        mbar_wait(&full[(gc + cneed) % NS], ((gc + cneed) / NS) & 1);
+                        if (!gs_wait(p, &full[(gc + cneed) % NS], ((gc + cneed) / NS) & 1))
+                            *abort_s = 1;
 #ifdef SB_GS_PROFILE
                         w_chunk += clock64() - tc;
 #endif
@@ -443,18 +488,22 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
                     }
                 }
                 named_bar_sync(1, C::NCOMP);
+                if (pos == POS_LEAD && *abort_s) return true;
                 if (!FULL && st == nsteps - 1) break;
             }
+            return false;
         };
         // full blocks: the trailing line (skew SMAX) is at column >= 1 at the
         // block's first step and the leading line at column <= ni at its last
         const bool tile_full = (J0 + C::BJ - 1 <= p.nj) && (K0 + C::BK - 1 <= p.nk);
-        for (int st0 = 0; st0 < nsteps; st0 += CW) {
+        bool aborted = false;
+        for (int st0 = 0; st0 < nsteps && !aborted; st0 += CW) {
             if (tile_full && st0 + 1 - SMAX >= 1 && st0 + CW <= ni && st0 + CW < nsteps)
-                block(st0, std::true_type{});
+                aborted = block(st0, std::true_type{});
             else
-                block(st0, std::false_type{});
+                aborted = block(st0, std::false_type{});
         }
+        if (aborted) break;
         if (tid == 0) {
             while (released < completed) mbar_arrive(&done[(gc + released++) % NS]);
         }
@@ -510,15 +559,26 @@ __global__ void gs_serial_kernel(double* g, int ni, int nj, int nk, int sweeps, 
 using GsC = GsCfg<16, 6, 16, 4, 1>;
 using GsC1 = GsCfg<16, 16, 16, 5, 1>;  // one CTA per SM (SB_GSCFG=1)
 
+// Per-device launch state (ticket/error words, progress flags, order table).
+// Launches on one device that use it are serialised whatever their stream:
+// each waits for `last` (recorded after the previous launch) and host-side
+// updates happen under `mu`, so concurrent sb_gs calls on two streams of one
+// device never share the counters of a running kernel.
 struct GsScratch {
+    std::mutex mu;
     int* words = nullptr;  // ticket, err
     int* prog = nullptr;
     size_t prog_cap = 0;
     int2* order = nullptr;
     size_t order_cap = 0;
     int tj = -1, tk = -1, ns = -1;
+    cudaEvent_t last = nullptr;
 };
 static GsScratch g_gs[16];
+
+// Test-only fault injection (sb_debug_fault): applies to later launches.
+static int g_fault = 0;
+static long long g_timeout = 1LL << 35;  // ~17 s at 1.9 GHz without progress
 #ifdef SB_GS_PROFILE
 static unsigned long long* g_gs_prof = nullptr;
 extern "C" void sb_gs_profile(unsigned long long* out) {
@@ -566,10 +626,15 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     if (dev >= 16) return fail(SB_ERR_CUDA, "device index %d unsupported", dev);
     GsScratch& S = g_gs[dev];
+    std::lock_guard<std::mutex> lk(S.mu);
     int* counters;
     int sms;
     int rc = get_counters(&counters, &sms);
     if (rc) return rc;
+    if (!S.last && (e = cudaEventCreateWithFlags(&S.last, cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "cudaEventCreate");
+    // the previous launch on this device (any stream) has finished with the scratch
+    if ((e = cudaStreamWaitEvent(st, S.last, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
 
     const int tiles_j = (nj + C::BJ - 1) / C::BJ, tiles_k = (nk + C::BK - 1) / C::BK;
     if (tiles_j > 32767 || tiles_k > 32767) return fail(SB_ERR_DIMENSION, "grid too large for GS tiling");
@@ -628,6 +693,8 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
     p.b = b;
     p.ticket = S.words;
     p.err = S.words + 1;
+    p.timeout = g_timeout;
+    p.fault = g_fault;
     p.prog = S.prog;
     p.order = S.order;
     p.grid = grid;
@@ -658,6 +725,7 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
         if (inter) kern_i<<<grid_ctas, C::NT, C::SMEM_BYTES, st>>>(lmap, smap, p);
         else kern_n<<<grid_ctas, C::NT, C::SMEM_BYTES, st>>>(lmap, smap, p);
         if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "gs launch");
+        if ((e = cudaEventRecord(S.last, st)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
         done += n;
     }
     return SB_OK;
@@ -673,17 +741,31 @@ int gs_serial_run(double* grid, int ni, int nj, int nk, int64_t iters, double b,
 // written), copied in and out with cudaMemcpy2D.  One scratch buffer per
 // device, grown on demand, stream-ordered like the rest of sb_gs.
 struct GsPitched {
+    std::mutex mu;
     double* buf = nullptr;
     size_t cap = 0;  // doubles
+    cudaEvent_t last = nullptr;  // after the previous user's copy-out (any stream)
 };
 static GsPitched g_gs_pitched[16];
 
-// frees the pitched-copy buffer of `dev` (caller synchronised the device)
-void gs_release(int dev) {
-    if (dev < 0 || dev >= 16) return;
-    if (g_gs_pitched[dev].buf) cudaFree(g_gs_pitched[dev].buf);
-    g_gs_pitched[dev].buf = nullptr;
-    g_gs_pitched[dev].cap = 0;
+// frees the pitched-copy buffer of `dev` (caller synchronised the device);
+// true if there was one
+bool gs_release(int dev) {
+    if (dev < 0 || dev >= 16) return false;
+    GsPitched& P = g_gs_pitched[dev];
+    std::lock_guard<std::mutex> lk(P.mu);
+    const bool had = P.buf != nullptr;
+    if (P.buf) cudaFree(P.buf);
+    P.buf = nullptr;
+    P.cap = 0;
+    return had;
+}
+
+// true if `dev` holds buffers that sb_release_caches would free
+bool gs_holds(int dev) {
+    if (dev < 0 || dev >= 16) return false;
+    std::lock_guard<std::mutex> lk(g_gs_pitched[dev].mu);
+    return g_gs_pitched[dev].buf != nullptr;
 }
 
 static int gs_run_pitched(double* grid, int ni, int nj, int nk, int64_t iters, double b,
@@ -693,6 +775,10 @@ static int gs_run_pitched(double* grid, int ni, int nj, int nk, int64_t iters, d
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     if (dev >= 16) return fail(SB_ERR_CUDA, "device index %d unsupported", dev);
     GsPitched& P = g_gs_pitched[dev];
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (!P.last && (e = cudaEventCreateWithFlags(&P.last, cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "cudaEventCreate");
+    if ((e = cudaStreamWaitEvent(st, P.last, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
     const int64_t nip = ni + 2, pitch = (nip + 1) / 2 * 2, rows = int64_t(nj + 2) * (nk + 2);
     const size_t need = size_t(pitch) * size_t(rows);
     if (P.cap < need) {
@@ -714,6 +800,7 @@ static int gs_run_pitched(double* grid, int ni, int nj, int nk, int64_t iters, d
     if ((e = cudaMemcpy2DAsync(grid, nip * 8, P.buf, pitch * 8, nip * 8, rows,
                                cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
         return cuda_fail(e, "cudaMemcpy2DAsync(out)");
+    if ((e = cudaEventRecord(P.last, st)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
     return SB_OK;
 }
 
@@ -778,6 +865,15 @@ extern "C" int sb_gs(double* grid, int64_t ni, int64_t nj, int64_t nk, int64_t i
     if (reinterpret_cast<uintptr_t>(grid) & 7) return fail(SB_ERR_ARGUMENT, "grid must be 8-byte aligned");
     if (iters == 0) return SB_OK;
     return gs_run(grid, (int)ni, (int)nj, (int)nk, iters, b, kernel, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int sb_debug_fault(int kind, int64_t timeout_cycles) {
+    using namespace sb;
+    clear_error();
+    if (kind < 0 || kind > 1) return fail(SB_ERR_ARGUMENT, "unknown fault kind %d", kind);
+    g_fault = kind;
+    g_timeout = timeout_cycles > 0 ? timeout_cycles : (1LL << 35);
+    return SB_OK;
 }
 
 extern "C" int sb_sync(void* stream) {

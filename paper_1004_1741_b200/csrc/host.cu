@@ -53,6 +53,7 @@ extern "C" {
 int sb_run_host(int kernel, double* host_grid, int64_t ni, int64_t nj, int64_t nk, int64_t iters,
                 double a, double b, int depth, int device) {
     clear_error();
+    DeviceGuard guard;
     int rc = check_dims(ni, nj, nk);
     if (rc) return rc;
     if (iters < 0) return fail(SB_ERR_PLAN, "iter_end must be >= 0, got %lld", (long long)iters);
@@ -146,10 +147,17 @@ static void batch_free(BatchCtx& B) {
 int sb_release_caches(int device) {
     clear_error();
     const int ndev = sb_device_count();
-    int cur = 0;
-    if (ndev > 0 && cudaGetDevice(&cur) != cudaSuccess) return fail(SB_ERR_CUDA, "cudaGetDevice");
+    if (ndev <= 0) return SB_OK;
+    DeviceGuard guard;
     for (int d = 0; d < std::min(ndev, 64); ++d) {
         if (device >= 0 && d != device) continue;
+        bool holds;
+        {
+            std::lock_guard<std::mutex> lk(g_host_mu);
+            holds = g_batch[d].nslots > 0 || g_host[d].g || g_host[d].s;
+        }
+        // devices without cached buffers are not touched (no new contexts)
+        if (!holds && !gs_holds(d) && !jacobi_holds(d)) continue;
         cudaError_t e = cudaSetDevice(d);
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return cuda_fail(e, "sb_release_caches");
@@ -163,13 +171,13 @@ int sb_release_caches(int device) {
         gs_release(d);
         jacobi_release(d);
     }
-    if (ndev > 0) cudaSetDevice(cur);
     return SB_OK;
 }
 
 int sb_run_host_batch(int kernel, double* const* host_grids, int count, int64_t ni, int64_t nj,
                       int64_t nk, int64_t iters, double a, double b, int depth, int device) {
     clear_error();
+    DeviceGuard guard;
     int rc = check_dims(ni, nj, nk);
     if (rc) return rc;
     if (iters < 0) return fail(SB_ERR_PLAN, "iter_end must be >= 0, got %lld", (long long)iters);
@@ -311,6 +319,7 @@ int sb_jacobi_slabs(int nslabs, const int* devices, double* const* slabs, double
                     int64_t ni, int64_t nj, int64_t nk, int64_t iters, double a, double b, int depth,
                     void* const* streams, int* result_in_scratch) {
     clear_error();
+    DeviceGuard guard;
     int rc = check_dims(ni, nj, nk);
     if (rc) return rc;
     if (iters < 0) return fail(SB_ERR_PLAN, "iter_end must be >= 0, got %lld", (long long)iters);
@@ -460,6 +469,7 @@ int sb_gs_slab_layout(int64_t nk, int nslabs, int slab, int64_t* own_lo, int64_t
 int sb_gs_slabs(int nslabs, const int* devices, double* const* slabs, int64_t ni, int64_t nj,
                 int64_t nk, int64_t iters, double b, int kernel, void* const* streams) {
     clear_error();
+    DeviceGuard guard;
     int rc = check_dims(ni, nj, nk);
     if (rc) return rc;
     if (iters < 0) return fail(SB_ERR_PLAN, "iter_end must be >= 0, got %lld", (long long)iters);

@@ -491,22 +491,34 @@ constexpr int kMaxFusedDepth = 4;
 // padded to an even number of doubles (outside the tensor maps' extent, so
 // never touched), copied in with cudaMemcpy2D and the result copied back
 // into a_buf.  Two scratch buffers per device, grown on demand.
+// Calls on two streams of one device are serialised through `last`.
 struct JacPitched {
     double* buf[2] = {nullptr, nullptr};
     size_t cap = 0;  // doubles per buffer
+    cudaEvent_t last = nullptr;  // after the previous user's copy-out (any stream)
 };
 static JacPitched g_jac_pitched[64];
 static std::mutex g_jac_pitched_mu;
 
-// frees the pitched-copy buffers of `dev` (caller synchronised the device)
-void jacobi_release(int dev) {
-    if (dev < 0 || dev >= 64) return;
+// frees the pitched-copy buffers of `dev` (caller synchronised the device);
+// true if there were any
+bool jacobi_release(int dev) {
+    if (dev < 0 || dev >= 64) return false;
     std::lock_guard<std::mutex> lk(g_jac_pitched_mu);
+    bool had = false;
     for (double*& q : g_jac_pitched[dev].buf) {
+        had = had || q;
         if (q) cudaFree(q);
         q = nullptr;
     }
     g_jac_pitched[dev].cap = 0;
+    return had;
+}
+
+bool jacobi_holds(int dev) {
+    if (dev < 0 || dev >= 64) return false;
+    std::lock_guard<std::mutex> lk(g_jac_pitched_mu);
+    return g_jac_pitched[dev].buf[0] != nullptr;
 }
 
 static int jacobi_run_pitched(double* a_buf, int ni, int nj, int nk, int64_t iters, double a,
@@ -517,6 +529,9 @@ static int jacobi_run_pitched(double* a_buf, int ni, int nj, int nk, int64_t ite
     if (dev >= 64) return fail(SB_ERR_CUDA, "device index %d unsupported", dev);
     std::lock_guard<std::mutex> lk(g_jac_pitched_mu);
     JacPitched& P = g_jac_pitched[dev];
+    if (!P.last && (e = cudaEventCreateWithFlags(&P.last, cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "cudaEventCreate");
+    if ((e = cudaStreamWaitEvent(st, P.last, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
     const int64_t nip = ni + 2, pitch = (nip + 1) / 2 * 2, rows = int64_t(nj + 2) * (nk + 2);
     const size_t need = size_t(pitch) * size_t(rows);
     if (P.cap < need) {
@@ -548,6 +563,7 @@ static int jacobi_run_pitched(double* a_buf, int ni, int nj, int nk, int64_t ite
     if ((e = cudaMemcpy2DAsync(a_buf, nip * 8, src, pitch * 8, nip * 8, rows,
                                cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
         return cuda_fail(e, "cudaMemcpy2DAsync(out)");
+    if ((e = cudaEventRecord(P.last, st)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
     return SB_OK;
 }
 

@@ -22,6 +22,23 @@ inline const char* tune_env(const char* name) {
 
 int fail(int code, const char* fmt, ...);
 
+// Restores the caller's current device when an entry point that switches
+// devices returns (any path).
+struct DeviceGuard {
+    int dev = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&dev) != cudaSuccess) {
+            cudaGetLastError();
+            dev = -1;
+        }
+    }
+    ~DeviceGuard() {
+        if (dev >= 0) cudaSetDevice(dev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 // Resident CTAs per SM of `kern` on the current device, with its dynamic
 // shared-memory opt-in made first.  The opt-in is a property of each
 // device's context, so it is made once per (kernel, device) -- not once per
@@ -52,7 +69,10 @@ std::vector<int4> build_item_list(int T, int tiles_i, int tiles_j, const std::ve
 int item_list(int T, int tiles_i, int tiles_j, const std::vector<char>& border, int kfirst,
               int klast, int grid, int kb, const int4** out, int* count);
 
-void gs_release(int dev);
-void jacobi_release(int dev);
+// free the per-device buffers kept between calls; true if there were any
+bool gs_release(int dev);
+bool jacobi_release(int dev);
+bool gs_holds(int dev);
+bool jacobi_holds(int dev);
 
 }  // namespace sb

@@ -138,3 +138,12 @@ def test_release_caches_without_device_is_a_no_op():
     lib = _lib.load()
     if _lib.device_count() == 0:
         assert lib.sb_release_caches(-1) == 0
+
+
+def test_debug_fault_hook_validates_its_arguments():
+    """sb_debug_fault (fault-injection test hook) needs no device; an unknown
+    kind is an argument error, 0 restores normal operation."""
+    lib = _lib.load()
+    with pytest.raises(ValueError):
+        _lib.check(lib.sb_debug_fault(7, 0))
+    _lib.check(lib.sb_debug_fault(0, 0))
