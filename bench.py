@@ -110,21 +110,23 @@ def dist_env():
     return world, rank, local
 
 
-def synth_slab(torch, eng, dev):
-    """Deterministic synthetic field over global plane index (consistent
-    across ranks, so ghosts equal the neighbours' owned planes): values in
-    [0, 1), zero Dirichlet halo -- the shape/value distribution of config 4."""
-    nkl2 = eng.nkl + 2
-    k = torch.arange(eng.k0, eng.k0 + nkl2, device=dev, dtype=torch.float64)[:, None, None]
-    j = torch.arange(NJ + 2, device=dev, dtype=torch.float64)[None, :, None]
-    i = torch.arange(NI + 2, device=dev, dtype=torch.float64)[None, None, :]
-    x = torch.frac(torch.sin(k * 12.9898 + j * 78.233 + i * 37.719) * 43758.5453).abs()
-    x[:, 0], x[:, -1], x[:, :, 0], x[:, :, -1] = 0.0, 0.0, 0.0, 0.0
+def seeded_slab(torch, eng, dev, chunk=64):
+    """The reference's config-4 input restricted to this rank's slab (plus
+    ghosts): create_grid(1024, 1024, 1024*N, seeded_random(42)) -- PCG64
+    seed 42, U[0,1), zero Dirichlet halo (reference grid.py:115-121) --
+    generated plane block by plane block (grid.seeded_planes advances the
+    stream), so no rank builds the global grid.  Its 100-sweep result at
+    N=1 is pinned to the reference's own hash (tests/golden/hashes.json
+    cfg4_jacobi1024_it100, tests/test_gpu_parity.py)."""
+    from paper_1004_1741_b200.grid import seeded_planes
+
     nk_total = NK_PER_GPU * eng.world
-    if eng.k0 == 0:
-        x[0] = 0.0
-    if eng.k0 + nkl2 - 1 == nk_total + 1:
-        x[-1] = 0.0
+    nkl2 = eng.nkl + 2
+    x = torch.empty((nkl2, NJ + 2, NI + 2), dtype=torch.float64, device=dev)
+    for p0 in range(0, nkl2, chunk):
+        p1 = min(nkl2, p0 + chunk)
+        blk = seeded_planes(42, NI, NJ, nk_total, eng.k0 + p0, eng.k0 + p1)
+        x[p0:p1].copy_(torch.from_numpy(blk))
     return x
 
 
@@ -141,35 +143,108 @@ def cpu_sample_n():
     return 512
 
 
-def cpu_grid(n):
-    import numpy as np
+def cpu_grid(n, lo=0.0, hi=1.0):
+    """create_grid(n, n, n, seeded_random(42, lo, hi)).data (host)."""
+    from paper_1004_1741_b200.grid import seeded_planes
 
-    g = np.random.default_rng(42).random((n + 2, n + 2, n + 2))
-    g[0], g[-1], g[:, 0], g[:, -1], g[:, :, 0], g[:, :, -1] = 0, 0, 0, 0, 0, 0
-    return g
+    return seeded_planes(42, n, n, n, 0, n + 2, lo, hi)
 
 
-def cpu_reference_rate(budget_s=12.0, n=None, threads=None, g=None, sweeps=None):
-    """The reference's CPU path (oracle port of the threaded k-slab Jacobi
-    engine, reference sweeps/threaded.py:28-59) on the host cores: a bounded
-    sample of the workload (n^3 interior, S sweeps sized to ~budget_s)."""
+def outer_cache_bytes():
+    """Size of the outermost CPU cache (sysfs), None if unknown."""
+    best = None
+    for idx in sorted(Path("/sys/devices/system/cpu/cpu0/cache").glob("index*")):
+        try:
+            text = (idx / "size").read_text().strip().upper()
+            val = int(text.rstrip("KMG")) * {"K": 1 << 10, "M": 1 << 20, "G": 1 << 30}.get(text[-1], 1)
+            best = val if best is None or val > best else best
+        except (OSError, ValueError):
+            continue
+    return best
+
+
+def choose_blocks(t, ni, nj, groups):
+    """reference sweeps/plan.py:123-149 (choose_block_size): smallest B whose
+    per-group wavefront working set (3t+2 padded planes of one j-block)
+    fits in half the outermost cache, clamped to [groups, nj]."""
+    cache = outer_cache_bytes()
+    if not cache:
+        return groups
+    for b in range(max(groups, 1), nj + 1):
+        if (3 * t + 2) * (ni + 2) * (-(-nj // b) + 2) * 8 <= cache / 2:
+            return b
+    return nj
+
+
+def cpu_variants(kernel, threads):
+    """The reference's CPU engines for `kernel` on `threads` host threads
+    (threaded/pipeline with P = cores, wavefront with t in
+    {2, 4, P}; Jacobi needs even t)."""
+    out = [("threaded" if kernel == "jacobi" else "pipeline", {"threads": threads})]
+    for t in sorted({2, 4, threads}):
+        if t > threads or threads % t or (kernel == "jacobi" and t % 2):
+            continue
+        out.append((f"wavefront(N={threads // t},t={t})", {"groups": threads // t, "tpg": t}))
+    return out
+
+
+def time_cpu_variant(kernel, name, kw, g, sweeps, a, b):
+    """Seconds of `sweeps` sweeps of one reference CPU engine (oracle port)."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle  # CPU baseline only
 
+    n = g.shape[0] - 2
+    if name.startswith("wavefront"):
+        t = kw["tpg"]
+        sweeps = max(t, sweeps - sweeps % t)
+        return oracle.time_variant(kernel, "wavefront", g, sweeps, a, b, groups=kw["groups"], tpg=t,
+                                   blocks=choose_blocks(t, n, n, kw["groups"])), sweeps
+    return oracle.time_variant(kernel, "threaded", g, sweeps, a, b, threads=kw["threads"]), sweeps
+
+
+def cpu_best(kernel, g, budget_s, a=0.0, b=1 / 6, threads=None):
+    """Every reference CPU engine for `kernel` timed on a bounded sample of
+    `g` (each about budget_s / #variants of sweeps, calibrated by a short
+    run); returns the best, named, with all variants' rates."""
+    threads = threads or os.cpu_count() or 1
+    n = g.shape[0] - 2
+    cells = n ** 3
+    variants = cpu_variants(kernel, threads)
+    per = budget_s / len(variants)
+    rates, plan = {}, {}
+    for name, kw in variants:
+        sec, sw = time_cpu_variant(kernel, name, kw, g, kw.get("tpg", 2), a, b)  # calibration
+        want = int(max(1, min(400, per * (sw * cells / sec) / cells)))
+        sec, sw = time_cpu_variant(kernel, name, kw, g, want, a, b)
+        rates[name] = sw * cells / sec / 1e6
+        plan[name] = (kw, sw)
+    best = max(rates, key=rates.get)
+    return best, rates, plan
+
+
+def cpu_reference_rate(budget_s=12.0, n=None, threads=None, g=None):
+    """The reference's CPU path on the host cores: every engine for config
+    4's Jacobi (threaded k-slabs, wavefront temporal blocking; oracle/ C
+    ports pinned to the reference) on a bounded sample of the headline grid
+    (n^3, seeded input), best reported and named; plus config 5's GS
+    (512^3 U[-1,1): pipeline and wavefront engines) under "gs"."""
     threads = threads or os.cpu_count() or 1
     if g is None:
-        n = n or cpu_sample_n()
-        g = cpu_grid(n)
+        g = cpu_grid(n or cpu_sample_n())
     n = g.shape[0] - 2
-    if sweeps is None:
-        calib = oracle.time_threaded_jacobi(g, 2, 0.0, 1 / 6, threads=threads) / 2
-        sweeps = int(max(2, min(200, budget_s / max(calib, 1e-6))))
-    sec = oracle.time_threaded_jacobi(g, sweeps, 0.0, 1 / 6, threads=threads)
-    return {"value": sweeps * n ** 3 / sec / 1e6, "unit": "MLUP/s", "cores": threads,
-            "kind": "port",
-            "sample": f"{n}^3 interior, {sweeps} Jacobi sweeps (sweep time only; grid copy and "
-                      f"scratch allocated beforehand), oracle port of the reference's threaded "
-                      f"k-slab engine on {threads} host threads"}
+    best, rates, plan = cpu_best("jacobi", g, budget_s, threads=threads)
+    del g
+    g5 = cpu_grid(512, -1.0, 1.0)
+    gbest, grates, gplan = cpu_best("gs-naive", g5, budget_s * 0.75, threads=threads)
+    del g5
+    return {"value": rates[best], "unit": "MLUP/s", "cores": threads, "kind": "port",
+            "variant": best, "variants": rates,
+            "sample": f"{n}^3 interior (seeded create_grid input), {plan[best][1]} Jacobi sweeps per "
+                      f"variant sample, each reference CPU engine (C ports of sweeps/threaded.py and "
+                      f"sweeps/wavefront.py) on {threads} host threads, sweep time only; best: {best}",
+            "gs": {"value": grates[gbest], "unit": "MLUP/s", "variant": gbest, "variants": grates,
+                   "sample": f"config 5: 512^3 U[-1,1), gs-naive, {gplan[gbest][1]} sweeps per "
+                             f"variant sample on {threads} host threads"}}
 
 
 def arm_config(world, depth):
@@ -178,38 +253,48 @@ def arm_config(world, depth):
                         "z-slabs + halo exchange",
             "ni": NI, "nj": NJ, "nk": NK_PER_GPU * world, "sweeps_per_step": SWEEPS,
             "depth": depth, "coeffs": [0.0, 1 / 6],
+            "input": "create_grid seeded_random(42): PCG64, U[0,1), zero Dirichlet halo",
             "parallelism": f"z-slabs x{world}" if world > 1 else "1 GPU",
             "l2": "inputs larger than L2 (8.6 GB/GPU per buffer)"}
 
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference_arm(args):
-    """The reference's CPU implementation of the path (the oracle port of its
-    threaded engine; the reference package is Python/numba and is not on the
-    GPU box) on all host threads, on this arm's config and metric: each step
-    times a bounded sample of the workload (the headline grid when it fits
-    in host memory, S sweeps sized so the run ends within minutes)."""
+    """The reference's CPU implementation of the path (C ports of its
+    engines, pinned bit for bit to the reference; the reference package is
+    Python/numba and is not on the GPU box) on all host threads, on this
+    arm's config and metric.  The warm-up times every engine on the sample
+    and picks the fastest (named in cpu_baseline.variant); each timed step
+    is then a bounded sample of the workload with that engine (the headline
+    grid when it fits in host memory)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    threads = os.cpu_count() or 1
     g = cpu_grid(cpu_sample_n())
-    rates = []
-    budget = max(4.0, min(15.0, 120.0 / max(1, args.steps + args.warmup)))
-    r = cpu_reference_rate(budget_s=budget, g=g)  # calibrates the sample's sweep count
-    sweeps = int(r["sample"].split(" Jacobi sweeps")[0].split()[-1])
+    n = g.shape[0] - 2
+    per_step = max(4.0, min(15.0, 120.0 / max(1, args.steps + args.warmup)))
+    best, rates, plan = cpu_best("jacobi", g, per_step * 2, threads=threads)
+    kw, sw_cal = plan[best]
+    per_variant = per_step * 2 / len(rates)  # what the calibration sample took
+    sweeps = max(1, int(sw_cal * per_step / per_variant))
+    out = []
     for step in range(args.warmup + args.steps):
-        r = cpu_reference_rate(g=g, sweeps=sweeps)
+        sec, sw = time_cpu_variant("jacobi", best, kw, g, sweeps, 0.0, 1 / 6)
         if step >= args.warmup:
-            rates.append(r["value"])
-    value = statistics.median(rates)
-    cfg = arm_config(world, args.depth)
-    cfg["cpu_sample"] = r["sample"]
+            out.append(sw * n ** 3 / sec / 1e6)
+    value = statistics.median(out)
+    cpu = {"value": value, "unit": "MLUP/s", "cores": threads, "kind": "port", "variant": best,
+           "variants": rates,
+           "sample": f"{n}^3 interior (seeded create_grid input), {sw} Jacobi sweeps per step with "
+                     f"the fastest reference CPU engine ({best}; C port pinned to the reference) "
+                     f"on {threads} host threads, sweep time only"}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "MLUP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": cfg,
-            "cpu_baseline": dict(r, value=value),
+            "config": arm_config(world, args.depth),
+            "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": "MLUP/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -219,8 +304,7 @@ def run_reference_arm(args):
 def time_gs(torch, lib, n, iters, kid, reps=2):
     from paper_1004_1741_b200 import _lib
 
-    g = torch.rand((n + 2, n + 2, n + 2), dtype=torch.float64, device="cuda") * 2 - 1
-    g[0], g[-1], g[:, 0], g[:, -1], g[:, :, 0], g[:, :, -1] = 0, 0, 0, 0, 0, 0
+    g = torch.from_numpy(cpu_grid(n, -1.0, 1.0)).cuda()  # config 5: seeded U[-1,1), halo 0
     st = torch.cuda.current_stream()
     sp = ctypes.c_void_p(st.cuda_stream)
     _lib.check(lib.sb_gs(g.data_ptr(), n, n, n, 2, 1 / 6, kid, sp))
@@ -242,7 +326,7 @@ def time_gs(torch, lib, n, iters, kid, reps=2):
 def time_jacobi_depths(torch, lib, n, iters, depths):
     from paper_1004_1741_b200 import _lib
 
-    g = torch.rand((n + 2, n + 2, n + 2), dtype=torch.float64, device="cuda")
+    g = torch.from_numpy(cpu_grid(n)).cuda()  # config 3: seeded U[0,1), Dirichlet halo 1.0
     g[0], g[-1], g[:, 0], g[:, -1], g[:, :, 0], g[:, :, -1] = 1, 1, 1, 1, 1, 1
     s = torch.empty_like(g)
     st = torch.cuda.current_stream()
@@ -308,7 +392,7 @@ def run_gpu_arm(args):
     nk_total = NK_PER_GPU * world
     eng = SlabEngine(NI, NJ, nk_total, depth, rank, world, gpu_compute(NI, NJ, 0.0, 1.0 / 6.0),
                      like=torch.empty(0, dtype=torch.float64, device=dev))
-    x = synth_slab(torch, eng, dev)
+    x = seeded_slab(torch, eng, dev)
     eng.bufs[0].copy_(x)
     eng.bufs[1].copy_(x)
     del x
@@ -429,7 +513,8 @@ def run_gpu_arm(args):
         line = {"metric": METRIC, "value": value, "unit": "MLUP/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec / args.steps * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (deterministic sin-hash field in [0,1), zero Dirichlet halo)",
+                "data": "synthetic (the reference's seeded create_grid input: PCG64 seed 42, U[0,1), "
+                        "zero Dirichlet halo)",
                 "config": arm_config(world, depth),
                 "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "clocks": clk.summary(), "also": also}

@@ -281,6 +281,22 @@ int sb_gs_slab_layout(int64_t nk, int nslabs, int slab, int64_t* own_lo, int64_t
 int sb_gs_slabs(int nslabs, const int* devices, double* const* slabs, int64_t ni, int64_t nj,
                 int64_t nk, int64_t iters, double b, int kernel, void* const* streams);
 
+/*
+ * Multi-GPU host entry: the reference `run(plan, g)` with a threaded plan
+ * spread over GPUs -- run_threaded_jacobi's k-slabs (sweeps/threaded.py:
+ * 28-59, partition_blocks at :39) and run_pipeline_gs's pipelined order
+ * (:62-96) with one z-slab per entry of devices[0..ndev) (an index may
+ * repeat: those slabs share the GPU).  `grid` is the whole padded grid in
+ * host memory or in any device's memory (UVA), updated in place with the
+ * final field.  Scatters the slabs (with ghost planes), runs sb_jacobi_slabs
+ * (`depth` sweeps per halo exchange, capped at the thinnest slab) or
+ * sb_gs_slabs, gathers the owned planes back; slab buffers are allocated
+ * for the call and freed before it returns.  Synchronous.  Bitwise equal to
+ * sb_run_host.  SB_ERR_PARTITION when ndev > nk.
+ */
+int sb_run_multi(int kernel, double* grid, int64_t ni, int64_t nj, int64_t nk, int64_t iters,
+                 double a, double b, int depth, int ndev, const int* devices);
+
 #ifdef __cplusplus
 }
 #endif

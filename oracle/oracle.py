@@ -43,6 +43,8 @@ def load():
     lib.sbo_run_threaded_jacobi.restype = i32
     lib.sbo_run_pipeline_gs.argtypes = [i32, vp, i64, i64, i64, i64, dbl, i32]
     lib.sbo_run_pipeline_gs.restype = i32
+    lib.sbo_run_wavefront.argtypes = [i32, vp, i64, i64, i64, i64, dbl, dbl, i32, i32, i32]
+    lib.sbo_run_wavefront.restype = i64
     for name in ("sbo_gs_window", "sbo_gs_window_interleaved"):
         getattr(lib, name).argtypes = [vp, vp, vp, i64, dbl, i64, i64]
         getattr(lib, name).restype = None
@@ -89,6 +91,53 @@ def run_threaded(kernel, data, iters, a=0.0, b=1.0 / 6.0, threads=None):
     if rc < 0:
         raise ValueError("partition error")
     return g
+
+
+def run_wavefront(kernel, data, iters, a=0.0, b=1.0 / 6.0, groups=1, tpg=2, blocks=None):
+    """Wavefront temporal blocking (reference sweeps/wavefront.py:127-376):
+    `groups` x `tpg` host threads, `blocks` j-blocks (default: groups).
+    Returns (new array with the final field, barrier phases)."""
+    g = np.array(data, dtype=np.float64, order="C", copy=True)
+    ni, nj, nk = _check(g)
+    blocks = blocks or groups
+    phases = load().sbo_run_wavefront(KERNEL_IDS[kernel], g.ctypes.data, ni, nj, nk, iters, a, b,
+                                      groups, tpg, blocks)
+    if phases < 0:
+        raise ValueError("plan error (iters % t, odd t for Jacobi, or blocks outside [1, nj])")
+    return g, phases
+
+
+def time_variant(kernel, variant, data, iters, a=0.0, b=1.0 / 6.0, threads=None, groups=None,
+                 tpg=None, blocks=None):
+    """Seconds spent in `iters` sweeps of `data` by one reference CPU engine
+    (variant "threaded": k-slab Jacobi / pipeline GS on `threads`;
+    "wavefront": `groups` x `tpg` threads over `blocks` j-blocks), setup
+    excluded (working copies allocated and touched first) -- the CPU
+    baseline legs of bench.py."""
+    import time
+
+    g = np.array(data, dtype=np.float64, order="C", copy=True)
+    ni, nj, nk = _check(g)
+    lib = load()
+    kid = KERNEL_IDS[kernel]
+    if variant == "wavefront":
+        blocks = blocks or groups
+        t0 = time.perf_counter()
+        rc = lib.sbo_run_wavefront(kid, g.ctypes.data, ni, nj, nk, iters, a, b, groups, tpg, blocks)
+    elif kernel == "jacobi":
+        scratch = g.copy()
+        threads = max(1, min(threads or os.cpu_count() or 1, nk))
+        t0 = time.perf_counter()
+        rc = lib.sbo_run_threaded_jacobi(g.ctypes.data, scratch.ctypes.data, ni, nj, nk, iters, a,
+                                         b, threads)
+    else:
+        threads = max(1, min(threads or os.cpu_count() or 1, nj))
+        t0 = time.perf_counter()
+        rc = lib.sbo_run_pipeline_gs(kid, g.ctypes.data, ni, nj, nk, iters, b, threads)
+    sec = time.perf_counter() - t0
+    if rc < 0:
+        raise ValueError("plan/partition error")
+    return sec
 
 
 def time_threaded_jacobi(data, iters, a=0.0, b=1.0 / 6.0, threads=None):

@@ -63,6 +63,8 @@ SIGNATURES = {
     "sb_gs_slab_layout": (_int, [_i64, _int, _int, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "sb_gs_slabs": (_int, [_int, ctypes.POINTER(_int), ctypes.POINTER(_vp), _i64, _i64, _i64, _i64,
                            _dbl, _int, ctypes.POINTER(_vp)]),
+    "sb_run_multi": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _dbl, _dbl, _int, _int,
+                            ctypes.POINTER(_int)]),
 }
 
 _lib = None

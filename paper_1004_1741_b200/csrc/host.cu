@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -549,6 +550,128 @@ int sb_gs_slabs(int nslabs, const int* devices, double* const* slabs, int64_t ni
         for (cudaEvent_t ev : {S[g].done, S[g].got_lo, S[g].got_hi}) cudaEventDestroy(ev);
     }
     return rc;
+}
+
+// The whole `run(plan, g)` contract over several GPUs: the grid (host or
+// device memory, UVA) is cut into z-slabs per partition_blocks, one per
+// entry of `devices`, scattered (with ghost planes), swept by the slab
+// drivers above and gathered back.  The multi-GPU form of the reference's
+// run_threaded_jacobi (k-slabs, threaded.py:28-59) and run_pipeline_gs
+// (pipelined stages, threaded.py:62-96).
+int sb_run_multi(int kernel, double* grid, int64_t ni, int64_t nj, int64_t nk, int64_t iters,
+                 double a, double b, int depth, int ndev, const int* devices) {
+    clear_error();
+    DeviceGuard guard;
+    int rc = check_dims(ni, nj, nk);
+    if (rc) return rc;
+    if (iters < 0) return fail(SB_ERR_PLAN, "iter_end must be >= 0, got %lld", (long long)iters);
+    if (kernel < SB_KERNEL_JACOBI || kernel > SB_KERNEL_GS_INTERLEAVED)
+        return fail(SB_ERR_PLAN, "unknown kernel %d", kernel);
+    const bool jac = (kernel == SB_KERNEL_JACOBI);
+    if (jac && (depth < 1 || depth > sb_max_depth()))
+        return fail(SB_ERR_PLAN, "depth must be in [1, %d], got %d", sb_max_depth(), depth);
+    if (!grid || !devices) return fail(SB_ERR_ARGUMENT, "null pointer");
+    if (ndev < 1) return fail(SB_ERR_ARGUMENT, "need at least one device, got %d", ndev);
+    if (ndev > nk)
+        return fail(SB_ERR_PARTITION, "cannot split nk=%lld planes into %d slabs", (long long)nk, ndev);
+    const int visible = sb_device_count();
+    if (visible < 1) return fail(SB_ERR_NODEVICE, "no CUDA device");
+    for (int s = 0; s < ndev; ++s)
+        if (devices[s] < 0 || devices[s] >= visible)
+            return fail(SB_ERR_ARGUMENT, "device %d out of range (%d visible)", devices[s], visible);
+    if (iters == 0) return SB_OK;
+    // ghost width: the requested depth, capped by the thinnest inner slab
+    // (results are identical for every depth)
+    int T = 1;
+    if (jac) {
+        T = depth;
+        if (ndev > 1) T = (int)std::min<int64_t>(T, nk / ndev);
+        if (ni % 2) T = 1;  // the slab blocks have no pitched path (odd rows: one sweep each)
+        T = std::max(T, 1);
+    }
+    const int64_t plane = (ni + 2) * (nj + 2);
+    const size_t pbytes = size_t(plane) * sizeof(double);
+    struct Part {
+        int64_t lo, hi, glo, ghi, nkl;  // owned global padded planes; ghosts; local interior planes
+        double* buf[2] = {nullptr, nullptr};
+    };
+    std::vector<Part> P(ndev);
+    std::vector<int> devs(devices, devices + ndev);
+    std::vector<cudaStream_t> st(ndev, nullptr);
+    std::vector<cudaStream_t> dev_stream(visible, nullptr);  // one stream per device (GS needs it)
+    cudaError_t e = cudaSuccess;
+    auto cleanup = [&]() {
+        for (int s = 0; s < ndev; ++s) {
+            cudaSetDevice(devs[s]);
+            for (double* p : P[s].buf)
+                if (p) cudaFree(p);
+        }
+        for (int d = 0; d < visible; ++d)
+            if (dev_stream[d]) {
+                cudaSetDevice(d);
+                cudaStreamDestroy(dev_stream[d]);
+            }
+    };
+    struct Cleanup {
+        std::function<void()> f;
+        ~Cleanup() { f(); }
+    } on_exit{cleanup};
+    for (int s = 0; s < ndev; ++s) {
+        Part& X = P[s];
+        if (jac) {
+            if ((rc = sb_slab_layout(nk, ndev, s, T, &X.lo, &X.hi, &X.glo, &X.ghi))) return rc;
+        } else {
+            if ((rc = sb_gs_slab_layout(nk, ndev, s, &X.lo, &X.hi))) return rc;
+            X.glo = X.ghi = 1;
+        }
+        X.nkl = (X.hi - X.lo) + X.glo + X.ghi - 2;
+        if ((e = cudaSetDevice(devs[s])) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+        if (!dev_stream[devs[s]] &&
+            (e = cudaStreamCreateWithFlags(&dev_stream[devs[s]], cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(e, "cudaStreamCreate");
+        st[s] = dev_stream[devs[s]];
+        const size_t bytes = size_t(X.nkl + 2) * pbytes;
+        for (int i = 0; i < (jac ? 2 : 1); ++i)
+            if ((e = cudaMalloc(&X.buf[i], bytes)) != cudaSuccess)
+                return cuda_fail(e, "cudaMalloc(slab)");
+        // scatter: global planes [lo-glo, hi+ghi) (UVA: host or any device)
+        if ((e = cudaMemcpyAsync(X.buf[0], grid + (X.lo - X.glo) * plane, bytes, cudaMemcpyDefault,
+                                 st[s])) != cudaSuccess)
+            return cuda_fail(e, "scatter copy");
+    }
+    std::vector<double*> b0(ndev), b1(ndev);
+    std::vector<void*> sv(ndev);
+    for (int s = 0; s < ndev; ++s) {
+        b0[s] = P[s].buf[0];
+        b1[s] = P[s].buf[1];
+        sv[s] = st[s];
+    }
+    int in_s = 0;
+    if (jac)
+        rc = sb_jacobi_slabs(ndev, devs.data(), b0.data(), b1.data(), ni, nj, nk, iters, a, b, T,
+                             sv.data(), &in_s);
+    else
+        rc = sb_gs_slabs(ndev, devs.data(), b0.data(), ni, nj, nk, iters, b, kernel, sv.data());
+    if (rc) return rc;
+    // gather the owned planes back into the caller's grid
+    for (int s = 0; s < ndev; ++s) {
+        const Part& X = P[s];
+        cudaSetDevice(devs[s]);
+        if ((e = cudaMemcpyAsync(grid + X.lo * plane, X.buf[in_s] + X.glo * plane,
+                                 size_t(X.hi - X.lo) * pbytes, cudaMemcpyDefault, st[s])) != cudaSuccess)
+            return cuda_fail(e, "gather copy");
+    }
+    for (int s = 0; s < ndev; ++s) {
+        cudaSetDevice(devs[s]);
+        if ((e = cudaStreamSynchronize(st[s])) != cudaSuccess) return cuda_fail(e, "gather");
+    }
+    if (!jac) {
+        for (int s = 0; s < ndev; ++s) {
+            cudaSetDevice(devs[s]);
+            if ((rc = gs_check_error(st[s]))) return rc;
+        }
+    }
+    return SB_OK;
 }
 
 }  // extern "C"

@@ -381,10 +381,15 @@ static int with_cfg(int T, F&& f) {
         case 2: SB_L(2, 4, 8, 8, 1, false, true);
         case 3: SB_L(3, 4, 8, 8, 1, false, true);
         case 4: SB_L(4, 4, 8, 8, 1, false, true);
+        // depths 5-8 (the slab path's ghost-zone blocks, the config-3 "steps
+        // per HBM pass" sweep): 12 warps x 2 rows; level 1 reads the TMA
+        // ring (L1S), level T stores through TMA (TS), one step loop (UNI) --
+        // the register-lean form (ptxas: 0 / 0 / 12 / 952 spill bytes at
+        // T = 5..8; the plain form spilled 0 / 156 / 6364 / 9736)
         case 5: SB_L(5, 2, 12, 3, 1);
-        case 6: SB_L(6, 2, 12, 3, 1);
-        case 7: SB_L(7, 2, 12, 3, 1);
-        case 8: SB_L(8, 2, 12, 3, 1);
+        case 6: SB_L(6, 2, 12, 3, 1, true, true, true);
+        case 7: SB_L(7, 2, 12, 3, 1, true, true, true);
+        case 8: SB_L(8, 2, 12, 3, 1, true, true, true);
     }
 #undef SB_L
     return fail(SB_ERR_PLAN, "unsupported depth %d", T);

@@ -178,15 +178,23 @@ class Measurement:
         return d
 
 
-def measure(plan, grid_factory, repetitions=5, warmup=1, device="cuda"):
+def measure(plan, grid_factory, repetitions=5, warmup=1, device="cuda", devices=None):
     """Run `plan` on identical fresh inputs (reference perf.py:241-297):
     `warmup` untimed runs, then `repetitions` timed ones.  Each input is
     created and moved to `device` outside the timed region; the timed region
     is the sweep call on the resident grid, bracketed by CUDA events on the
-    current stream.  MLUP/s from the median."""
+    current stream.  MLUP/s from the median.  With several `devices` (the
+    threaded engines' z-slabs across GPUs) the call is synchronous over all
+    of them and is timed by the host clock, slab scatter/gather included."""
+    import time
+
     import torch
 
     from .sweeps import resolve_depth, run
+    from .sweeps.engine import resolve_devices
+
+    devs = resolve_devices(devices)
+    multi = devs is not None and len(devs) > 1
 
     if repetitions < 1:
         raise ConfigError(f"need at least one repetition, got {repetitions}")
@@ -199,15 +207,17 @@ def measure(plan, grid_factory, repetitions=5, warmup=1, device="cuda"):
         torch.cuda.synchronize()
         st = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
         e0.record(st)
-        run(plan, g)
+        run(plan, g, devices=devs)
         e1.record(st)
         torch.cuda.synchronize()
+        t1 = time.perf_counter()
         if rep >= warmup:
-            seconds.append(e0.elapsed_time(e1) / 1e3)
+            seconds.append((t1 - t0) if multi else e0.elapsed_time(e1) / 1e3)
     med = median(seconds)
     total = plan.iter_end * g.ni * g.nj * g.nk
-    cfg = {"threads": plan.threads}
+    cfg = {"threads": plan.threads, "gpus": len(devs) if multi else 1}
     if plan.config is not None:
         cfg.update(num_groups=plan.config.num_groups,
                    threads_per_group=plan.config.threads_per_group,

@@ -13,8 +13,23 @@ contribute is their contract: argument validation and exceptions
 Grids: ``g.data`` as a host numpy array goes through ``sb_run_host`` (copy
 in, sweep, copy out; synchronous).  As a CUDA float64 torch tensor it is
 swept in place on the current stream through ``sb_jacobi`` / ``sb_gs``.
-The result is always left in ``g.data`` and ``g`` is returned.
+
+Returned grid (reference sweeps/serial.py:24-31, threaded.py:41-59): the
+serial and threaded Jacobi engines ping-pong ``g`` and ``g.copy()``, so for
+an odd ``iter_end`` they return the copy holding the final field and leave
+``g`` at sweep ``iter_end - 1``; every other engine returns ``g`` itself.
+
+Several GPUs: the threaded engines (``run_threaded_jacobi``, and
+``run_pipeline_gs`` for the GS kernels) take ``devices`` -- a sequence of
+CUDA device indices, an int N (the first N GPUs) or "all"; default the
+``SB200_DEVICES`` environment variable (same forms), else one GPU.  With
+more than one device the grid is cut into z-slabs (the reference's
+``partition_blocks(nk, P)`` k-slabs, threaded.py:39), one per device, and
+runs through ``sb_run_multi``: Jacobi with per-time-block halo exchange,
+GS as the exact cross-GPU z-pipeline.  Bitwise equal to one GPU.
 """
+
+import os
 
 import ctypes
 
@@ -105,6 +120,48 @@ def execute(kernel, g, iters, a, b, depth, sync=True):
     return g
 
 
+def resolve_devices(devices=None):
+    """GPUs for the threaded engines: a list of CUDA device indices, or None
+    for the single-GPU path.  `devices`: a sequence of indices, an int N (the
+    first N visible GPUs) or "all"; None reads $SB200_DEVICES ("0,1,2,3",
+    "4" or "all")."""
+    if devices is None:
+        env = os.environ.get("SB200_DEVICES", "").strip()
+        if not env:
+            return None
+        devices = env
+    if isinstance(devices, str):
+        text = devices.strip().lower()
+        if text == "all":
+            devices = _lib.device_count()
+        elif "," in text:
+            devices = [int(x) for x in text.split(",") if x.strip()]
+        else:
+            devices = int(text)
+    if isinstance(devices, int):
+        if devices < 1:
+            raise ValueError(f"need at least one GPU, got {devices}")
+        return list(range(devices))
+    out = [int(d) for d in devices]
+    if not out:
+        raise ValueError("empty device list")
+    return out
+
+
+def barrier_phases(plan, depth):
+    """Device-wide synchronisation points of the GPU run -- the counterpart
+    of the reference wavefront engines' stats["barrier_phases"] (one barrier
+    per plane phase, wavefront.py:308-311): kernel-launch boundaries.  A
+    Jacobi run is ceil(iter_end / depth) fused launches (passes); a GS run
+    is one launch per call (its sweeps are pipelined inside)."""
+    if plan.iter_end == 0:
+        return 0
+    if plan.kernel != JACOBI:
+        return 1
+    eff = depth if depth <= 4 else 4  # sb_jacobi fuses at most 4 per pass
+    return -(-plan.iter_end // eff)
+
+
 def _finish(plan, g, stats, **extra):
     if stats is not None:
         stats["line_updates"] = plan.iter_end * g.nk * g.nj
@@ -120,35 +177,127 @@ def _run(plan, g, stats, **extra):
         return g
     depth = resolve_depth(plan, g)
     execute(plan.kernel, g, plan.iter_end, plan.coeffs.a, plan.coeffs.b, depth)
-    return _finish(plan, g, stats, depth=depth, **extra)
+    return _finish(plan, g, stats, depth=depth, barrier_phases=barrier_phases(plan, depth), **extra)
+
+
+def _run_pingpong(plan, g, stats, devs=None, **extra):
+    """Jacobi engines that own two grids (serial, threaded): for an odd
+    iter_end the final field is returned in a new grid (the reference's
+    g.copy()) and g holds sweep iter_end - 1."""
+    n = plan.iter_end
+    if n == 0:
+        if stats is not None:
+            stats["line_updates"] = 0
+        return g
+    depth = resolve_depth(plan, g)
+    sweep = (lambda grid, k: _execute_multi(plan.kernel, grid, k, plan.coeffs.a, plan.coeffs.b,
+                                            depth, devs)) if devs else \
+        (lambda grid, k: execute(plan.kernel, grid, k, plan.coeffs.a, plan.coeffs.b, depth))
+    out = g
+    if n % 2 == 0:
+        sweep(g, n)
+    else:
+        if n > 1:
+            sweep(g, n - 1)
+        out = g.copy()
+        sweep(out, 1)
+    phases = barrier_phases(plan, depth) + (1 if n % 2 and n > 1 else 0)
+    _finish(plan, g, stats, depth=depth, barrier_phases=phases, **extra)
+    return out
+
+
+def _execute_multi(kernel, g, iters, a, b, depth, devices):
+    """`iters` sweeps of g across `devices` (z-slabs, sb_run_multi); g may
+    be a host numpy grid or a CUDA tensor on any device.  Synchronous."""
+    lib = _lib.load()
+    _lib.require_device()
+    data = g.data
+    if _is_torch(data):
+        import torch
+
+        if not data.is_cuda or data.dtype != torch.float64 or not data.is_contiguous():
+            raise ValueError("device grids must be contiguous float64 CUDA tensors")
+        if tuple(data.shape) != g.shape_padded:
+            raise ValueError(f"grid data shape {tuple(data.shape)} != {g.shape_padded}")
+        torch.cuda.current_stream(data.device).synchronize()  # the library uses its own streams
+        ptr = data.data_ptr()
+    else:
+        if not (isinstance(data, np.ndarray) and data.dtype == np.float64
+                and data.flags.c_contiguous and data.flags.writeable):
+            raise ValueError("host grids must be writeable C-contiguous float64 numpy arrays")
+        if data.shape != g.shape_padded:
+            raise ValueError(f"grid data shape {data.shape} != {g.shape_padded}")
+        ptr = data.ctypes.data
+    devs = (ctypes.c_int * len(devices))(*devices)
+    _lib.check(lib.sb_run_multi(_lib.KERNEL_IDS[kernel], ptr, g.ni, g.nj, g.nk, iters, a, b,
+                                depth, len(devices), devs))
+    return g
+
+
+def _multi(devices):
+    devs = resolve_devices(devices)
+    return devs if devs is not None and len(devs) > 1 else None
 
 
 def run_serial(plan, g, stats=None):
-    """reference sweeps/serial.py:8-42 (the result is left in g)."""
+    """reference sweeps/serial.py:8-42."""
+    if plan.kernel == JACOBI:
+        return _run_pingpong(plan, g, stats)
     return _run(plan, g, stats)
 
 
-def run_threaded_jacobi(plan, g, placement=None, stats=None):
-    """reference sweeps/threaded.py:28-59: same checks; z-slab parallelism
-    is the CTA grid (and the multi-GPU slab engine)."""
+def run_threaded_jacobi(plan, g, placement=None, stats=None, devices=None):
+    """reference sweeps/threaded.py:28-59: same checks and returned grid;
+    z-slab parallelism is the CTA grid on one GPU, or z-slabs across
+    `devices` (module docstring) with halo exchange between time blocks."""
     if plan.kernel != JACOBI:
         raise PlanError(f"threaded engine is Jacobi-only, got kernel {plan.kernel!r}")
     if plan.threads > g.nk:
         raise PartitionError(f"{plan.threads} threads cannot split nk={g.nk} planes")
-    return _run(plan, g, stats, pinned=None)
+    devs = _multi(devices)
+    if devs is not None and len(devs) > g.nk:
+        raise PartitionError(f"{len(devs)} GPUs cannot split nk={g.nk} planes")
+    extra = {"pinned": None}
+    if devs is not None:
+        extra.update(devices=devs, slabs=len(devs))
+    return _run_pingpong(plan, g, stats, devs, **extra)
 
 
-def run_pipeline_gs(plan, g, placement=None, stats=None):
+def run_pipeline_gs(plan, g, placement=None, stats=None, devices=None):
     """reference sweeps/threaded.py:62-96: exact lexicographic order, here
-    as the flag-pipelined tile wavefront."""
+    as the flag-pipelined tile wavefront on one GPU, or the cross-GPU
+    z-pipeline of slabs over `devices`."""
     if plan.kernel == JACOBI:
         raise PlanError("pipeline engine applies to Gauss-Seidel kernels only")
     if plan.threads > g.nj:
         raise PartitionError(f"{plan.threads} threads cannot split nj={g.nj} lines")
-    out = _run(plan, g, stats, pinned=None)
-    if stats is not None and plan.iter_end:
-        stats["stages_per_sweep"] = g.nk + plan.threads - 1
-    return out
+    devs = _multi(devices)
+    if devs is not None and len(devs) > g.nk:
+        raise PartitionError(f"{len(devs)} GPUs cannot split nk={g.nk} planes")
+    if plan.iter_end == 0:
+        if stats is not None:
+            stats["line_updates"] = 0
+        return g
+    if devs is None:
+        out = _run(plan, g, stats, pinned=None)
+        if stats is not None:
+            stats["stages_per_sweep"] = gs_stages_per_sweep(g, plan.iter_end)
+        return out
+    _execute_multi(plan.kernel, g, plan.iter_end, 0.0, plan.coeffs.b, 1, devs)
+    # z-pipeline: a sweep of G slabs takes G stages to pass through
+    # (sweep s of slab g runs once slab g-1 finished sweep s)
+    return _finish(plan, g, stats, depth=1, pinned=None, devices=devs, slabs=len(devs),
+                   stages_per_sweep=len(devs), barrier_phases=plan.iter_end + len(devs) - 1)
+
+
+def gs_stages_per_sweep(g, iters):
+    """Hyperplane stages of one GS sweep on the GPU: tiles of 16 j-lines x
+    BK k-planes (gs.cu: BK = 16 for calls of one or two sweeps, else 6) run
+    along anti-diagonals J + K, so a sweep passes through
+    tiles_j + tiles_k - 1 stages -- the counterpart of the reference
+    pipeline's nk + P - 1 (threaded.py:81)."""
+    bk = 16 if iters <= 2 else 6
+    return -(-g.nj // 16) + -(-g.nk // bk) - 1
 
 
 def _wavefront_checks(plan, g):
@@ -176,17 +325,18 @@ def run_wavefront_gs(plan, g, placement=None, stats=None, instrument=False):
     return run_wavefront(plan, g, placement, stats, instrument)
 
 
-def run(plan, g, placement=None, stats=None, instrument=False):
+def run(plan, g, placement=None, stats=None, instrument=False, devices=None):
     """reference sweeps/__init__.py:52-71: variant dispatch; a GS kernel on
-    the threaded variant runs the pipeline engine."""
+    the threaded variant runs the pipeline engine.  `devices` (or
+    $SB200_DEVICES) spreads the threaded/pipeline engines over GPUs."""
     if plan.variant == SERIAL:
         return run_serial(plan, g, stats=stats)
     if plan.variant == THREADED:
         if plan.kernel == JACOBI:
-            return run_threaded_jacobi(plan, g, placement=placement, stats=stats)
-        return run_pipeline_gs(plan, g, placement=placement, stats=stats)
+            return run_threaded_jacobi(plan, g, placement=placement, stats=stats, devices=devices)
+        return run_pipeline_gs(plan, g, placement=placement, stats=stats, devices=devices)
     if plan.variant == PIPELINE:
-        return run_pipeline_gs(plan, g, placement=placement, stats=stats)
+        return run_pipeline_gs(plan, g, placement=placement, stats=stats, devices=devices)
     if plan.variant == WAVEFRONT:
         return run_wavefront(plan, g, placement=placement, stats=stats, instrument=instrument)
     raise PlanError(f"unknown variant {plan.variant!r}")

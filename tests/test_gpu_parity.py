@@ -45,6 +45,10 @@ def test_small_cases_host_path(small_cases):
 
 @pytest.mark.parametrize("depth", [1, 2, 3, 4, 5, 8])
 def test_small_cases_device_path_every_depth(small_cases, depth):
+    """sb_jacobi at every accepted depth request: 1-4 fuse that many sweeps
+    per pass; requests of 5-8 run as 4-sweep passes (sb_jacobi's cap, see
+    include/stencil_b200.h) -- the genuinely fused 5-8 kernels are checked
+    by test_fused_deep_blocks_vs_oracle and test_config3_true_depth8."""
     for name, (rec, want) in small_cases.items():
         a, b = coeffs_of(rec)
         got = run_device(rec["kernel"], make_input(rec["spec"]).data, rec["iters"], a, b, depth)
@@ -91,6 +95,54 @@ def test_random_shapes_vs_oracle():
         for depth in ((1, 3, 8) if kernel == "jacobi" else (1,)):
             got = run_device(kernel, data, iters, a, b, depth)
             assert sha(got) == sha(want), (ni, nj, nk, kernel, iters, depth)
+
+
+def _planes(src, dst, k_lo, k_hi, sweeps, a, b):
+    lib = _lib.load()
+    nk, nj, ni = (x - 2 for x in src.shape)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _lib.check(lib.sb_jacobi_planes(src.data_ptr(), dst.data_ptr(), ni, nj, nk, k_lo, k_hi, sweeps,
+                                    a, b, st))
+    _lib.check(lib.sb_sync(st))
+
+
+@pytest.mark.parametrize("sweeps", [5, 6, 7, 8])
+def test_fused_deep_blocks_vs_oracle(sweeps):
+    """The genuinely fused 5-8 sweep kernels (one HBM pass; sb_jacobi_planes,
+    the slab path's ghost-zone block) == the oracle, whole grid and a
+    partial output range, several tile counts and boundary cases."""
+    for (ni, nj, nk), (a, b) in ((( 96, 41, 29), (0.0, 1 / 6)), ((50, 13, 40), (0.5, 0.1)),
+                                 ((144, 60, 9), (0.2, 0.13))):
+        data = make_input({"shape": [ni, nj, nk], "pattern": "random", "seed": ni + sweeps,
+                           "lo": -1.0, "hi": 1.0}).data
+        want = oracle.run_serial("jacobi", data, sweeps, a, b)
+        src = torch.from_numpy(data).cuda()
+        dst = src.clone()
+        _planes(src, dst, 1, nk + 1, sweeps, a, b)
+        assert sha(dst.cpu().numpy()) == sha(want), (ni, nj, nk, sweeps)
+        # partial output range: only planes [k_lo, k_hi) written, exact there
+        k_lo, k_hi = 1 + nk // 4, 1 + (3 * nk) // 4
+        dst = src.clone()
+        _planes(src, dst, k_lo, k_hi, sweeps, a, b)
+        got = dst.cpu().numpy()
+        assert np.array_equal(got[k_lo:k_hi], want[k_lo:k_hi]), (ni, nj, nk, sweeps)
+        assert np.array_equal(got[:k_lo], data[:k_lo]) and np.array_equal(got[k_hi:], data[k_hi:])
+
+
+def test_config3_true_depth8_vs_reference_hash(hashed_cases):
+    """BASELINE config 3 at "8 steps per HBM pass": 512^3 x 100 as twelve
+    genuinely fused 8-sweep passes plus one 4-sweep pass (100 = 12 x 8 + 4),
+    == the reference's own result."""
+    rec = hashed_cases["cfg3_jacobi512_halo1_it100"]
+    a, b = coeffs_of(rec)
+    bufs = [torch.from_numpy(make_input(rec["spec"]).data).cuda()]
+    bufs.append(bufs[0].clone())
+    n = rec["spec"]["shape"][2]
+    cur = 0
+    for sweeps in [8] * 12 + [4]:
+        _planes(bufs[cur], bufs[cur ^ 1], 1, n + 1, sweeps, a, b)
+        cur ^= 1
+    assert sha_device(bufs[cur]) == rec["output_sha256"]
 
 
 def test_run_batch_pipelined_host_path():

@@ -184,3 +184,77 @@ def test_line_api_argument_errors_without_device():
         jacobi_line_update(src, create_grid(6, 6, 6, InitPattern.uniform(0)), StencilCoeffs(0, 0.1), 6, 0)
     with pytest.raises(BoundsError):
         gs_line_update(src, 0.1, 0, -1)
+
+
+def test_resolve_devices_forms(monkeypatch):
+    from paper_1004_1741_b200.sweeps.engine import resolve_devices
+
+    monkeypatch.delenv("SB200_DEVICES", raising=False)
+    assert resolve_devices() is None
+    assert resolve_devices(3) == [0, 1, 2]
+    assert resolve_devices([2, 0, 2]) == [2, 0, 2]
+    assert resolve_devices("1,3") == [1, 3]
+    assert resolve_devices("2") == [0, 1]
+    monkeypatch.setenv("SB200_DEVICES", "0,0,1")
+    assert resolve_devices() == [0, 0, 1]
+    assert resolve_devices([5]) == [5]  # explicit argument wins over the environment
+    for bad in (0, [], "0,"[:0] or "-1"):
+        with pytest.raises(ValueError):
+            resolve_devices(bad)
+
+
+def test_multi_gpu_argument_errors_before_any_work(monkeypatch):
+    """More GPUs than planes is the reference's PartitionError for P > nk
+    (threaded.py:31-33), raised before a device is touched."""
+    monkeypatch.delenv("SB200_DEVICES", raising=False)
+    g = create_grid(4, 4, 3, InitPattern.seeded_random(1))
+    with pytest.raises(PartitionError):
+        run(SweepPlan("jacobi", "threaded", 2, threads=2), g, devices=[0, 0, 0, 0])
+    with pytest.raises(PartitionError):
+        run(SweepPlan("gs-naive", "pipeline", 2, threads=2), g, devices=4)
+    monkeypatch.setenv("SB200_DEVICES", "0,0,0,0")
+    with pytest.raises(PartitionError):
+        run_threaded_jacobi(SweepPlan("jacobi", "threaded", 2), g)
+    with pytest.raises(PlanError):
+        run_pipeline_gs(SweepPlan("jacobi", "pipeline", 2), g)
+
+
+def test_barrier_phase_counts():
+    from paper_1004_1741_b200.sweeps.engine import barrier_phases, gs_stages_per_sweep
+
+    assert barrier_phases(SweepPlan("jacobi", "serial", 0), 4) == 0
+    assert barrier_phases(SweepPlan("jacobi", "serial", 100), 4) == 25
+    assert barrier_phases(SweepPlan("jacobi", "serial", 10), 3) == 4
+    assert barrier_phases(SweepPlan("jacobi", "serial", 16), 8) == 4  # passes of at most 4
+    assert barrier_phases(SweepPlan("gs-naive", "serial", 100), 1) == 1
+    g = create_grid(8, 40, 30, InitPattern.uniform(0))
+    assert gs_stages_per_sweep(g, 100) == 3 + 5 - 1
+    assert gs_stages_per_sweep(g, 1) == 3 + 2 - 1
+
+
+def test_seeded_planes_equal_create_grid_slices():
+    from paper_1004_1741_b200.grid import seeded_planes
+
+    for (ni, nj, nk), (lo, hi) in (((7, 5, 9), (0.0, 1.0)), ((4, 6, 3), (-1.0, 1.0))):
+        full = create_grid(ni, nj, nk, InitPattern.seeded_random(42, lo, hi)).data
+        for p_lo, p_hi in ((0, nk + 2), (0, 1), (1, 4), (2, nk + 2), (nk + 1, nk + 2), (3, 3)):
+            got = seeded_planes(42, ni, nj, nk, p_lo, p_hi, lo, hi)
+            assert got.tobytes() == full[p_lo:p_hi].tobytes(), (ni, nj, nk, p_lo, p_hi)
+    with pytest.raises(BoundsError):
+        seeded_planes(42, 3, 3, 3, 2, 6)
+
+
+def test_multi_gpu_path_reaches_the_library_without_a_gpu(monkeypatch):
+    """On a CPU-only host the multi-GPU drop-in path fails loudly at the
+    device check (no CPU fallback) -- after all argument handling."""
+    import torch
+
+    from paper_1004_1741_b200.errors import DeviceError
+
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only check")
+    monkeypatch.delenv("SB200_DEVICES", raising=False)
+    g = create_grid(4, 4, 6, InitPattern.seeded_random(1))
+    for plan in (SweepPlan("jacobi", "threaded", 3, threads=2), SweepPlan("gs-naive", "pipeline", 2)):
+        with pytest.raises(DeviceError):
+            run(plan, g, devices=[0, 0])

@@ -65,3 +65,24 @@ def test_cli_verify_and_bench(capsys, tmp_path):
     rec = json.loads(out.read_text())
     assert rec["depth"] == 4 and rec["mlups"] > 0 and 0 < rec["hbm_frac"] < 5
     assert (tmp_path / "g.bin").stat().st_size == 24 + 64 ** 3 * 8
+
+
+@pytest.mark.gpu
+def test_cli_gpus_threaded_and_pipeline(capsys, tmp_path):
+    """--devices / --gpus run the threaded engines as z-slabs over GPUs
+    (one GPU here: slabs share it), checked bitwise against the serial
+    engine like the reference's verify (cli.py:297-331)."""
+    for kernel, variant in (("jacobi", "threaded"), ("gs-naive", "pipeline"),
+                            ("gs-interleaved", "threaded")):
+        assert main(["verify", "--kernel", kernel, "--variant", variant, "--iters", "7",
+                     "--size", "30x22x18", "--devices", "0,0,0"]) == 0
+    out = tmp_path / "r.json"
+    assert main(["bench", "--kernel", "jacobi", "--variant", "threaded", "--size", "64x64x64",
+                 "--iters", "8", "--reps", "2", "--devices", "0,0", "--format", "json",
+                 "--out", str(out)]) == 0
+    rec = json.loads(out.read_text())
+    assert rec["gpus"] == 2 and rec["mlups"] > 0
+
+
+def test_cli_gpus_argument_errors(capsys):
+    assert main(["verify", "--kernel", "jacobi", "--variant", "threaded", "--gpus", "0"]) == 2
