@@ -49,7 +49,8 @@ def test_small_cases_over_slabs_host_grids(small_cases, nslabs):
         stats = {}
         out = run(_plan(rec, a, b), g, devices=[0] * nslabs, stats=stats)
         assert sha(out.data) == sha(want), (name, nslabs)
-        assert stats["slabs"] == nslabs and stats["line_updates"] == rec["iters"] * g.nk * g.nj
+        assert stats["line_updates"] == rec["iters"] * g.nk * g.nj
+        assert rec["iters"] == 0 or stats["slabs"] == nslabs
         checked += 1
     assert checked > 10
 
