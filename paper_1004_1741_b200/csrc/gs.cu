@@ -41,6 +41,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <cstdlib>
 #include <mutex>
 #include <type_traits>
@@ -57,9 +58,46 @@ namespace sb {
 int make_grid_map3p(CUtensorMap* m, const double* base, int64_t nip, int64_t njp, int64_t nkp,
                     int bw, int bh, int bd, int64_t pitch);
 
+// Slabs.  A launch sweeps one grid, or several z-slabs of one global grid
+// (the cross-GPU z-pipeline, sb_gs_slabs): each slab is a local padded grid
+// whose planes 0 and nk+1 are ghost planes holding the neighbours' edge
+// planes.  Tile (J, 0) of a slab waits for the slab below to have pushed its
+// top plane's chunk (sweep s values: D) into the ghost plane below; tile
+// (J, last) for the slab above to have pushed its bottom plane's chunk
+// (sweep s-1 values: U) into the ghost plane above.  Pushes are plain
+// stores by the storer thread (to peer memory when the neighbour is on
+// another GPU), published by a system-scope release of a per-(sweep, J)
+// flag in the receiving slab's memory -- the same dependency protocol as
+// between tiles of one grid, so successive sweeps overlap across slabs (and
+// GPUs) as they do across tiles.  The write-after-read hazards on a ghost
+// plane are ordered by the chain that already exists: a neighbour's sweep
+// s+1 push of chunk c follows its sweep s+1 load of chunk c, which waited
+// for this slab's sweep s store (hence load) of chunk c.
+constexpr int kGsMaxSlabs = 8;
+struct GsSlab {
+    int nk;              // interior planes of the slab's local grid
+    int tiles_k;         // K tiles of the slab
+    int tile0;           // index of tile (0, 0) in the launch's progress arrays
+    int* ghost_lo;       // [R][tiles_j] progress of the ghost plane below (this slab's
+                         // memory, written by the neighbour below); null: Dirichlet plane
+    int* ghost_hi;       // [R][tiles_j] ghost plane above; null: Dirichlet plane
+    double* push_lo;     // the neighbour below's ghost plane above (its local plane nk+1)
+    double* push_hi;     // the neighbour above's ghost plane below (its local plane 0)
+    int* push_lo_flag;   // the neighbour below's ghost_hi
+    int* push_hi_flag;   // the neighbour above's ghost_lo
+    int lo_remote;       // the neighbour below / above runs on another GPU: its flags
+    int hi_remote;       // and pushes are ordered at system scope (else GPU scope)
+};
+struct GsMaps {
+    CUtensorMap ld[kGsMaxSlabs], st[kGsMaxSlabs];
+};
+
 struct GsParams {
-    int ni, nj, nk;
-    int tiles_j, tiles_k, ntiles;
+    int ni, nj;
+    int nslabs;
+    int64_t pitch;         // row pitch of every slab grid (doubles)
+    GsSlab slab[kGsMaxSlabs];
+    int tiles_j, ntiles;
     int nch;               // column chunks per line (ceil((ni+2)/CW))
     long long tasks;       // sweeps * ntiles
     double b;
@@ -68,8 +106,7 @@ struct GsParams {
     int* err;              // error word (timeout): every role polls it and exits
     long long timeout;     // cycles without progress before a wait gives up
     int fault;             // test-only fault injection (sb_debug_fault), 0 = none
-    const int2* order;     // ticket -> (sweep, J | K << 16), in wavefront order
-    double* grid;          // the grid
+    const int2* order;     // ticket -> (sweep | slab << 16, J | K << 16), in wavefront order
     unsigned long long* prof;  // SB_GS_PROFILE builds: per-CTA cycle counters
 };
 
@@ -97,7 +134,7 @@ struct GsCfg {
 };
 
 struct GsTask {
-    int s, J, K, tile;  // s < 0: stop
+    int s, J, K, tile, slab;  // s < 0: stop; K is slab-local
 };
 
 // progress encoding: (sweep+1) * (nch+1) + chunks_stored   (0 = nothing)
@@ -117,24 +154,34 @@ struct GsDeps {
     int want_base[6];  // prog_val(sweep, 0, nch) of the awaited sweep
     int seen[6];
     int n;
+    unsigned sys;      // bit k: entry k is a ghost flag written by another slab (system scope)
 };
 
 template <class C>
 __device__ __forceinline__ void deps_init(const GsParams& p, const GsTask& t, GsDeps& d) {
     d.n = 0;
-    auto add = [&](int s, int tile) {
-        d.addr[d.n] = p.prog + (s % C::R) * p.ntiles + tile;
+    d.sys = 0;
+    auto add_at = [&](const int* a, int s) {
+        d.addr[d.n] = a;
         d.want_base[d.n] = prog_val(s, 0, p.nch);
         d.seen[d.n] = 0;
         ++d.n;
     };
+    auto add = [&](int s, int tile) { add_at(p.prog + (s % C::R) * p.ntiles + tile, s); };
+    auto add_ghost = [&](const int* flags, int s, int remote) {
+        if (remote) d.sys |= 1u << d.n;
+        add_at(flags + (s % C::R) * p.tiles_j + t.J, s);
+    };
+    const GsSlab& S = p.slab[t.slab];
     if (t.s > 0) {
         add(t.s - 1, t.tile);
         if (t.J + 1 < p.tiles_j) add(t.s - 1, t.tile + 1);
-        if (t.K + 1 < p.tiles_k) add(t.s - 1, t.tile + p.tiles_j);
+        if (t.K + 1 < S.tiles_k) add(t.s - 1, t.tile + p.tiles_j);
+        else if (S.ghost_hi) add_ghost(S.ghost_hi, t.s - 1, S.hi_remote);  // U: slab above, s-1
     }
     if (t.J > 0) add(t.s, t.tile - 1);
     if (t.K > 0) add(t.s, t.tile - p.tiles_j);
+    else if (S.ghost_lo) add_ghost(S.ghost_lo, t.s, S.lo_remote);      // D: slab below, s
 }
 
 // true when chunk c of the task may be loaded; polls only stale entries
@@ -143,7 +190,7 @@ __device__ __forceinline__ bool deps_ready(GsDeps& d, int c) {
     for (int k = 0; k < d.n; ++k) {
         const int want = d.want_base[k] + c + 1;
         if (d.seen[k] < want) {
-            d.seen[k] = ld_acquire(d.addr[k]);
+            d.seen[k] = ((d.sys >> k) & 1) ? ld_acquire_sys(d.addr[k]) : ld_acquire(d.addr[k]);
             ok = ok && (d.seen[k] >= want);
         }
     }
@@ -155,14 +202,15 @@ __device__ __forceinline__ GsTask decode_task(const GsParams& p, long long tk) {
     GsTask t;
     if (tk >= p.tasks) {
         t.s = -1;
-        t.J = t.K = t.tile = 0;
+        t.J = t.K = t.tile = t.slab = 0;
         return t;
     }
     const int2 o = p.order[tk];
-    t.s = o.x;
+    t.s = o.x & 0xffff;
+    t.slab = o.x >> 16;
     t.J = o.y & 0xffff;
     t.K = o.y >> 16;
-    t.tile = t.K * p.tiles_j + t.J;
+    t.tile = p.slab[t.slab].tile0 + t.K * p.tiles_j + t.J;
     return t;
 }
 
@@ -205,7 +253,7 @@ __device__ void gs_loader_drain(uint64_t* full, uint32_t gload) {
 // ---------------------------------------------------------------------------
 // loader (one thread): dependency-checked chunk loads into free ring slots
 template <class C>
-__device__ void gs_loader(const CUtensorMap* ld_map, const GsParams& p, double* ring, uint64_t* full,
+__device__ void gs_loader(const GsMaps& maps, const GsParams& p, double* ring, uint64_t* full,
                           uint64_t* empty, GsTask* queue) {
     constexpr int NS = C::NS, CW = C::CW;
     const int nch = p.nch;
@@ -258,8 +306,8 @@ __device__ void gs_loader(const CUtensorMap* ld_map, const GsParams& p, double* 
             t0 = clock64();
             fence_proxy_async_global();
             mbar_arrive_expect_tx(&full[slot], C::BOX_BYTES);
-            tma_load_3d(ring + size_t(slot) * C::SLOT, ld_map, c * CW, lt.J * C::BJ, lt.K * C::BK,
-                        &full[slot]);
+            tma_load_3d(ring + size_t(slot) * C::SLOT, &maps.ld[lt.slab], c * CW, lt.J * C::BJ,
+                        lt.K * C::BK, &full[slot]);
         }
     }
 }
@@ -267,41 +315,121 @@ __device__ void gs_loader(const CUtensorMap* ld_map, const GsParams& p, double* 
 // storer (one thread): writes finished chunks back with TMA, frees the ring
 // slot as soon as the store has read shared memory, and publishes progress
 // once the data has landed in global memory
+// Copies row block [J0, J0+BJ) x chunk c of one tile plane (a line set of
+// a ring slot) into plane `dst` of a neighbour slab's grid (its ghost plane;
+// peer memory when the neighbour is on another GPU): the interior rows, the
+// chunk's columns inside the padded row.  One warp, 16-byte stores (the
+// chunk's first column and the row pitch are even).
 template <class C>
-__device__ void gs_storer(const CUtensorMap* st_map, const GsParams& p, double* ring, uint64_t* done,
+__device__ __forceinline__ void gs_push_plane(const GsParams& p, double* dst, const double* lines,
+                                              int J0, int c, int lane) {
+    constexpr int CW = C::CW, PAIRS = CW / 2;
+    const int col0 = c * CW;
+    const int ncol = min(CW, p.ni + 2 - col0);   // columns inside the padded row
+    const int nrow = min(C::BJ, p.nj + 1 - J0);  // interior rows of the tile
+    for (int idx = lane; idx < nrow * PAIRS; idx += 32) {
+        const int jl = idx / PAIRS, x = 2 * (idx % PAIRS);
+        if (x >= ncol) continue;
+        const double* src = lines + jl * CW + x;
+        double* out = dst + int64_t(J0 + jl) * p.pitch + col0 + x;
+        if (x + 1 < ncol) *reinterpret_cast<double2*>(out) = make_double2(src[0], src[1]);
+        else out[0] = src[0];
+    }
+}
+
+// storer (one warp; lane 0 drives the TMA stores and the flags): writes
+// finished chunks back with TMA, frees the ring slot as soon as the store has
+// read shared memory, and publishes progress once the data has landed in
+// global memory.  A tile holding a slab's edge plane also pushes that plane's
+// chunk into the neighbour slab's ghost plane (the whole warp) and releases
+// the neighbour's ghost flag.
+template <class C>
+__device__ void gs_storer(const GsMaps& maps, const GsParams& p, double* ring, uint64_t* done,
                           uint64_t* empty, uint64_t* full, GsTask* queue) {
     constexpr int NS = C::NS, CW = C::CW;
     const int nch = p.nch;
+    const int lane = threadIdx.x & 31;
     uint32_t gstore = 0;
     int sq = 0;
     long long t0 = clock64();
     while (true) {
         // the task's first chunk being loaded implies its queue entry is written
         const uint32_t slot0 = gstore % NS;
-        while (!mbar_try_wait(&full[slot0], (gstore / NS) & 1))
-            if (gs_abort(p, t0)) return;
-        const GsTask t = queue[sq];
+        int ab = 0;
+        GsTask t{};
+        if (lane == 0) {
+            while (!mbar_try_wait(&full[slot0], (gstore / NS) & 1))
+                if (gs_abort(p, t0)) {
+                    ab = 1;
+                    break;
+                }
+            if (!ab) t = queue[sq];
+        }
+        if (__shfl_sync(0xffffffffu, ab, 0)) return;
+        t.s = __shfl_sync(0xffffffffu, t.s, 0);
+        t.J = __shfl_sync(0xffffffffu, t.J, 0);
+        t.K = __shfl_sync(0xffffffffu, t.K, 0);
+        t.tile = __shfl_sync(0xffffffffu, t.tile, 0);
+        t.slab = __shfl_sync(0xffffffffu, t.slab, 0);
         sq = (sq + 1) % C::QS;
         if (t.s < 0) return;
+        const GsSlab& S = p.slab[t.slab];
         const int J0 = 1 + t.J * C::BJ, K0 = 1 + t.K * C::BK;
+        // owned planes of the tile: never store into the ghost plane above
+        // (a partial top tile's halo line), which the neighbour writes
+        const int nq = min(C::BK, S.nk + 1 - K0);
+        const bool push_hi = S.push_hi && t.K == S.tiles_k - 1;
+        const bool push_lo = S.push_lo && t.K == 0;
         int* flag = p.prog + (t.s % C::R) * p.ntiles + t.tile;
         for (int c = 0; c < nch; ++c, ++gstore) {
             const uint32_t slot = gstore % NS;
-            while (!mbar_try_wait(&done[slot], (gstore / NS) & 1))
-                if (gs_abort(p, t0)) return;
-            t0 = clock64();
             const double* base = ring + size_t(slot) * C::SLOT;
-            for (int q = 0; q < C::BK; ++q)
-                tma_store_3d(st_map, base + ((q + 1) * C::LJ + 1) * CW, c * CW, J0, K0 + q);
-            bulk_commit();
-            bulk_wait_read<0>();  // the slot's data has left shared memory
-            mbar_arrive(&empty[slot]);
-            bulk_wait<0>();       // ... and landed in global memory
-            fence_proxy_async_global();
-            // test-only fault (sb_debug_fault(1)): tile 0 never publishes
-            // sweep 0 past its first chunk, so its dependants time out
-            if (p.fault == 1 && t.s == 0 && t.tile == 0 && c >= 1) continue;
-            st_release(flag, prog_val(t.s, c + 1, nch));
+            if (lane == 0) {
+                while (!mbar_try_wait(&done[slot], (gstore / NS) & 1))
+                    if (gs_abort(p, t0)) {
+                        ab = 1;
+                        break;
+                    }
+                if (!ab) {
+                    t0 = clock64();
+                    for (int q = 0; q < nq; ++q)
+                        tma_store_3d(&maps.st[t.slab], base + ((q + 1) * C::LJ + 1) * CW, c * CW, J0,
+                                     K0 + q);
+                    bulk_commit();
+                }
+            }
+            if (__shfl_sync(0xffffffffu, ab, 0)) return;
+            if (push_hi)  // top owned plane -> the slab above's plane 0
+                gs_push_plane<C>(p, S.push_hi, base + (nq * C::LJ + 1) * CW, J0, c, lane);
+            if (push_lo)  // bottom plane -> the slab below's plane nk+1
+                gs_push_plane<C>(p, S.push_lo, base + (C::LJ + 1) * CW, J0, c, lane);
+            __syncwarp();  // the pushes have read the slot (and are ordered before lane 0's release)
+            if (lane == 0) {
+                bulk_wait_read<0>();  // the slot's data has left shared memory
+                mbar_arrive(&empty[slot]);
+                bulk_wait<0>();       // ... and landed in global memory
+                fence_proxy_async_global();
+                // test-only fault (sb_debug_fault(1)): tile 0 never publishes
+                // sweep 0 past its first chunk, so its dependants time out
+                if (p.fault == 1 && t.s == 0 && t.tile == 0 && c >= 1) continue;
+                const int v = prog_val(t.s, c + 1, nch);
+                st_release(flag, v);
+                if (push_hi || push_lo) {
+                    // the warp's pushes are ordered before these releases by the
+                    // __syncwarp above (releases are cumulative); a peer GPU
+                    // additionally needs the system-scope fence
+                    const int gi = (t.s % C::R) * p.tiles_j + t.J;
+                    if ((push_hi && S.hi_remote) || (push_lo && S.lo_remote)) __threadfence_system();
+                    if (push_hi) {
+                        if (S.hi_remote) st_release_sys(S.push_hi_flag + gi, v);
+                        else st_release(S.push_hi_flag + gi, v);
+                    }
+                    if (push_lo) {
+                        if (S.lo_remote) st_release_sys(S.push_lo_flag + gi, v);
+                        else st_release(S.push_lo_flag + gi, v);
+                    }
+                }
+            }
         }
     }
 }
@@ -374,9 +502,8 @@ __device__ __forceinline__ void gs_line_step(GsLine& L, double* smem, uint32_t g
 // ---------------------------------------------------------------------------
 template <class C, bool INTERLEAVED>
 __global__ void __launch_bounds__(C::NT, 1)
-gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
-               const __grid_constant__ CUtensorMap st_map, const GsParams p) {
-    constexpr int BJ = C::BJ, CW = C::CW, NS = C::NS, LJ = C::LJ, SMAX = C::SMAX;
+gs_tile_kernel(const __grid_constant__ GsMaps maps, const __grid_constant__ GsParams p) {
+    constexpr int BJ = C::BJ, CW = C::CW, NS = C::NS, SMAX = C::SMAX;
     extern __shared__ __align__(128) double smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(NS) * C::SLOT);
     uint64_t* done = full + NS;
@@ -397,11 +524,12 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
 
     if (tid >= C::NCOMP) {
         if (tid == C::NCOMP) {
-            tma_prefetch_desc(&ld_map);
-            gs_loader<C>(&ld_map, p, smem, full, empty, queue);
-        } else if (tid == C::NCOMP + 32) {
-            tma_prefetch_desc(&st_map);
-            gs_storer<C>(&st_map, p, smem, done, empty, full, queue);
+            for (int i = 0; i < p.nslabs; ++i) tma_prefetch_desc(&maps.ld[i]);
+            gs_loader<C>(maps, p, smem, full, empty, queue);
+        } else if (tid >= C::NCOMP + 32) {  // the storer warp
+            if (tid == C::NCOMP + 32)
+                for (int i = 0; i < p.nslabs; ++i) tma_prefetch_desc(&maps.st[i]);
+            gs_storer<C>(maps, p, smem, done, empty, full, queue);
         }
         return;
     }
@@ -441,11 +569,12 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
         q = (q + 1) % C::QS;
         if (t.s < 0) break;
         const int J0 = 1 + t.J * BJ, K0 = 1 + t.K * C::BK;
+        const int nk = p.slab[t.slab].nk;
         GsLine lines[LPT];
 #pragma unroll
         for (int l = 0; l < LPT; ++l) {
             const int kl = kl0 + l * KSTEP;
-            gs_line_init<C>(lines[l], smem, gc, jl, kl, (J0 + jl <= p.nj) && (K0 + kl <= p.nk));
+            gs_line_init<C>(lines[l], smem, gc, jl, kl, (J0 + jl <= p.nj) && (K0 + kl <= nk));
         }
         int ready = 1;               // chunks known loaded (thread 0)
         int completed = 0;           // chunks completed so far
@@ -495,7 +624,7 @@ gs_tile_kernel(const __grid_constant__ CUtensorMap ld_map,
         };
         // full blocks: the trailing line (skew SMAX) is at column >= 1 at the
         // block's first step and the leading line at column <= ni at its last
-        const bool tile_full = (J0 + C::BJ - 1 <= p.nj) && (K0 + C::BK - 1 <= p.nk);
+        const bool tile_full = (J0 + C::BJ - 1 <= p.nj) && (K0 + C::BK - 1 <= nk);
         bool aborted = false;
         for (int st0 = 0; st0 < nsteps && !aborted; st0 += CW) {
             if (tile_full && st0 + 1 - SMAX >= 1 && st0 + CW <= ni && st0 + CW < nsteps)
@@ -571,7 +700,7 @@ struct GsScratch {
     size_t prog_cap = 0;
     int2* order = nullptr;
     size_t order_cap = 0;
-    int tj = -1, tk = -1, ns = -1;
+    std::vector<int> key;  // what the uploaded order table describes
     cudaEvent_t last = nullptr;
 };
 static GsScratch g_gs[16];
@@ -587,18 +716,31 @@ extern "C" void sb_gs_profile(unsigned long long* out) {
 }
 #endif
 
-// Ticket order over `sweeps` sweeps of a tiles_j x tiles_k tile grid, in
-// windows of `window` sweeps: inside a window by tau = (J + K) + 2 * sweep,
-// then sweep, then J; windows one after another.  Every dependency of task
-// (s, J, K) -- (s, J-1, K), (s, J, K-1) at tau-1, (s-1, J+1, K), (s-1, J, K+1)
-// at tau-1, (s-1, J, K) at tau-2, (s-R+1, J, K) at tau-2(R-1), or an earlier
-// window -- has a smaller ticket, so a persistent grid cannot deadlock.
-// Successive sweeps advance together in a diagonal band (the paper's
-// multi-wavefront GS); the window bounds how many are in flight, so that a
-// tile's next sweep reads its previous sweep's data while it is still in L2.
-static std::vector<int2> wavefront_order(int tiles_j, int tiles_k, int sweeps, int window) {
+// Ticket order over `sweeps` sweeps of the tiles of one launch, in windows
+// of `window` sweeps: inside a window by tau = (J + K) + 2 * sweep, then
+// sweep, then J; windows one after another.  K is the tile's global K index
+// over all slabs of the grid (kt[g] = K tiles of slab g, in z order); only
+// tiles of slabs in this launch (mine[g] >= 0: its index in the launch) get
+// tickets.  Every dependency of task (s, J, K) -- (s, J-1, K), (s, J, K-1)
+// at tau-1, (s-1, J+1, K), (s-1, J, K+1) at tau-1, (s-1, J, K) at tau-2,
+// (s-R+1, J, K) at tau-2(R-1), or an earlier window -- has a smaller
+// (window, tau) key, in this launch or in another GPU's launch of the same
+// order: every device takes its tasks in key order, so the task with the
+// smallest unfinished key anywhere is always running -- no deadlock, on one
+// persistent grid or across GPUs.  Successive sweeps advance together in a
+// diagonal band (the paper's multi-wavefront GS); the window bounds how many
+// are in flight, so that a tile's next sweep reads its previous sweep's data
+// while it is still in L2.
+static std::vector<int2> wavefront_order(int tiles_j, const std::vector<int>& kt,
+                                         const std::vector<int>& mine, int sweeps, int window) {
+    std::vector<int> kslab, klocal;  // global K -> (slab, local K)
+    for (size_t g = 0; g < kt.size(); ++g)
+        for (int k = 0; k < kt[g]; ++k) {
+            kslab.push_back((int)g);
+            klocal.push_back(k);
+        }
+    const int tiles_k = (int)kslab.size();
     std::vector<int2> ord;
-    ord.reserve(size_t(sweeps) * tiles_j * tiles_k);
     const int dmax = tiles_j + tiles_k - 2;
     for (int s0 = 0; s0 < sweeps; s0 += window) {
         const int ns = std::min(window, sweeps - s0);
@@ -606,8 +748,11 @@ static std::vector<int2> wavefront_order(int tiles_j, int tiles_k, int sweeps, i
             for (int s = std::max(0, (tau - dmax + 1) / 2); s < ns && 2 * s <= tau; ++s) {
                 const int d = tau - 2 * s;
                 if (d > dmax) continue;
-                for (int J = std::max(0, d - (tiles_k - 1)); J < tiles_j && J <= d; ++J)
-                    ord.push_back(make_int2(s0 + s, J | ((d - J) << 16)));
+                for (int J = std::max(0, d - (tiles_k - 1)); J < tiles_j && J <= d; ++J) {
+                    const int Kg = d - J, g = kslab[Kg];
+                    if (mine[g] >= 0)
+                        ord.push_back(make_int2((s0 + s) | (mine[g] << 16), J | (klocal[Kg] << 16)));
+                }
             }
     }
     return ord;
@@ -618,13 +763,44 @@ static int gs_window() {
     return w;
 }
 
+// Host view of one slab of a launch (a single-grid call is one slab without
+// neighbours).
+struct GsLaunchSlab {
+    double* grid = nullptr;
+    int nk = 0;
+    int* ghost_lo = nullptr;
+    int* ghost_hi = nullptr;
+    double* push_lo = nullptr;
+    double* push_hi = nullptr;
+    int* push_lo_flag = nullptr;
+    int* push_hi_flag = nullptr;
+    int lo_remote = 0, hi_remote = 0;  // neighbour on another device
+};
+
+// Sweeps per launch: bounded by the order table size and the int32
+// progress encoding.
 template <class C>
-static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double b, bool inter,
-                     cudaStream_t st, int64_t pitch = 0) {
+static int64_t gs_batch_limit(int ni, int64_t ntiles) {
+    const int64_t nch64 = (ni + 2 + C::CW - 1) / C::CW;
+    return std::max<int64_t>(1, std::min<int64_t>(
+        std::min<int64_t>(512, ((int64_t(1) << 30) / (nch64 + 1)) - 2), (int64_t(1) << 26) / ntiles));
+}
+
+// Launches `iters` sweeps of the slabs sl[0..nsl) (all on the current
+// device; kt / mine: K tiles of every slab of the global grid and the
+// launch index of each, see wavefront_order) in batches of at most
+// gs_batch_limit sweeps.  reset_ghosts: zero the slabs' ghost flags before
+// each batch on `st` (when every neighbour is in this launch); cross-GPU
+// callers reset them themselves and pass one batch at a time.
+template <class C>
+static int gs_launch_slabs(const GsLaunchSlab* sl, int nsl, const std::vector<int>& kt,
+                           const std::vector<int>& mine, int ni, int nj, int64_t iters, double b,
+                           bool inter, cudaStream_t st, int64_t pitch, int window, bool reset_ghosts) {
     int dev;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     if (dev >= 16) return fail(SB_ERR_CUDA, "device index %d unsupported", dev);
+    if (nsl < 1 || nsl > kGsMaxSlabs) return fail(SB_ERR_ARGUMENT, "%d slabs in one launch", nsl);
     GsScratch& S = g_gs[dev];
     std::lock_guard<std::mutex> lk(S.mu);
     int* counters;
@@ -636,9 +812,13 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
     // the previous launch on this device (any stream) has finished with the scratch
     if ((e = cudaStreamWaitEvent(st, S.last, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
 
-    const int tiles_j = (nj + C::BJ - 1) / C::BJ, tiles_k = (nk + C::BK - 1) / C::BK;
-    if (tiles_j > 32767 || tiles_k > 32767) return fail(SB_ERR_DIMENSION, "grid too large for GS tiling");
-    const int ntiles = tiles_j * tiles_k;
+    const int tiles_j = (nj + C::BJ - 1) / C::BJ;
+    int ntiles = 0;
+    for (int i = 0; i < nsl; ++i) {
+        const int tk = (sl[i].nk + C::BK - 1) / C::BK;
+        if (tiles_j > 32767 || tk > 32767) return fail(SB_ERR_DIMENSION, "grid too large for GS tiling");
+        ntiles += tiles_j * tk;
+    }
     if (!S.words && (e = cudaMalloc(&S.words, 64 * sizeof(int))) != cudaSuccess)
         return cuda_fail(e, "cudaMalloc");
     const size_t need = size_t(C::R) * ntiles;
@@ -647,15 +827,16 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
         if ((e = cudaMalloc(&S.prog, need * sizeof(int))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
         S.prog_cap = need;
     }
-    // sweeps per launch: bounded by the order table size and the int32 progress encoding
-    const int64_t nch64 = (ni + 2 + C::CW - 1) / C::CW;
-    const int64_t per_launch = std::max<int64_t>(1, std::min<int64_t>(
-        std::min<int64_t>(512, ((int64_t(1) << 30) / (nch64 + 1)) - 2), (int64_t(1) << 26) / ntiles));
-    const int batch = (int)std::min<int64_t>(iters, per_launch);
-    if (S.tj != tiles_j || S.tk != tiles_k || S.ns != batch) {
-        const std::vector<int2> ord = wavefront_order(tiles_j, tiles_k, batch, gs_window());
+    const int batch = (int)std::min<int64_t>(iters, gs_batch_limit<C>(ni, ntiles));
+    auto upload_order = [&](int n) -> int {
+        std::vector<int> key = {tiles_j, window, n, C::BJ, C::BK};
+        key.insert(key.end(), kt.begin(), kt.end());
+        key.insert(key.end(), mine.begin(), mine.end());
+        if (key == S.key) return SB_OK;
+        const std::vector<int2> ord = wavefront_order(tiles_j, kt, mine, n, window);
         if (S.order_cap < ord.size()) {
             if (S.order) cudaFree(S.order);
+            S.order = nullptr;
             if ((e = cudaMalloc(&S.order, ord.size() * sizeof(int2))) != cudaSuccess)
                 return cuda_fail(e, "cudaMalloc(order)");
             S.order_cap = ord.size();
@@ -665,16 +846,35 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
                                  st)) != cudaSuccess)
             return cuda_fail(e, "cudaMemcpy(order)");
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "order upload");
-        S.tj = tiles_j;
-        S.tk = tiles_k;
-        S.ns = batch;
-    }
+        S.key = key;
+        return SB_OK;
+    };
 
-    CUtensorMap lmap, smap;
-    const int64_t nip = ni + 2, njp = nj + 2, nkp = nk + 2;
+    GsMaps maps;
+    GsParams p;
+    memset(&p, 0, sizeof p);
+    const int64_t nip = ni + 2, njp = nj + 2;
     if (pitch <= 0) pitch = nip;
-    if ((rc = make_grid_map3p(&lmap, grid, nip, njp, nkp, C::CW, C::LJ, C::LK, pitch))) return rc;
-    if ((rc = make_grid_map3p(&smap, grid, nip, njp, nkp, C::CW, C::BJ, 1, pitch))) return rc;
+    int tile0 = 0;
+    for (int i = 0; i < nsl; ++i) {
+        if ((rc = make_grid_map3p(&maps.ld[i], sl[i].grid, nip, njp, sl[i].nk + 2, C::CW, C::LJ, C::LK,
+                                  pitch)) ||
+            (rc = make_grid_map3p(&maps.st[i], sl[i].grid, nip, njp, sl[i].nk + 2, C::CW, C::BJ, 1, pitch)))
+            return rc;
+        GsSlab& X = p.slab[i];
+        X.nk = sl[i].nk;
+        X.tiles_k = (sl[i].nk + C::BK - 1) / C::BK;
+        X.tile0 = tile0;
+        tile0 += X.tiles_k * tiles_j;
+        X.ghost_lo = sl[i].ghost_lo;
+        X.ghost_hi = sl[i].ghost_hi;
+        X.push_lo = sl[i].push_lo;
+        X.push_hi = sl[i].push_hi;
+        X.push_lo_flag = sl[i].push_lo_flag;
+        X.push_hi_flag = sl[i].push_hi_flag;
+        X.lo_remote = sl[i].lo_remote;
+        X.hi_remote = sl[i].hi_remote;
+    }
 
     auto kern_n = gs_tile_kernel<C, false>;
     auto kern_i = gs_tile_kernel<C, true>;
@@ -682,12 +882,11 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
     if ((rc = ctas_per_sm((const void*)kern_i, C::NT, C::SMEM_BYTES, &occ)) ||
         (rc = ctas_per_sm((const void*)kern_n, C::NT, C::SMEM_BYTES, &occ)))
         return rc;
-    GsParams p;
     p.ni = ni;
     p.nj = nj;
-    p.nk = nk;
+    p.nslabs = nsl;
+    p.pitch = pitch;
     p.tiles_j = tiles_j;
-    p.tiles_k = tiles_k;
     p.ntiles = ntiles;
     p.nch = (ni + 2 + C::CW - 1) / C::CW;
     p.b = b;
@@ -696,8 +895,6 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
     p.timeout = g_timeout;
     p.fault = g_fault;
     p.prog = S.prog;
-    p.order = S.order;
-    p.grid = grid;
     p.prof = nullptr;
 #ifdef SB_GS_PROFILE
     static unsigned long long* prof = nullptr;
@@ -706,29 +903,40 @@ static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double
     p.prof = prof;
     g_gs_prof = prof;
 #endif
+    const size_t gbytes = size_t(C::R) * tiles_j * sizeof(int);
     for (int64_t done = 0; done < iters;) {
         const int n = (int)std::min<int64_t>(iters - done, batch);
-        if (n != S.ns) {  // a shorter final batch needs its own order table
-            const std::vector<int2> ord = wavefront_order(tiles_j, tiles_k, n, gs_window());
-            if ((e = cudaMemcpyAsync(S.order, ord.data(), ord.size() * sizeof(int2), cudaMemcpyHostToDevice,
-                                     st)) != cudaSuccess)
-                return cuda_fail(e, "cudaMemcpy(order)");
-            if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "order upload");
-            S.ns = n;
-        }
+        if ((rc = upload_order(n))) return rc;
+        p.order = S.order;
         p.tasks = (long long)n * ntiles;
         if ((e = cudaMemsetAsync(S.words, 0, 64 * sizeof(int), st)) != cudaSuccess)
             return cuda_fail(e, "memset");
         if ((e = cudaMemsetAsync(S.prog, 0, need * sizeof(int), st)) != cudaSuccess)
             return cuda_fail(e, "memset");
+        if (reset_ghosts)
+            for (int i = 0; i < nsl; ++i)
+                for (int* gf : {sl[i].ghost_lo, sl[i].ghost_hi})
+                    if (gf && (e = cudaMemsetAsync(gf, 0, gbytes, st)) != cudaSuccess)
+                        return cuda_fail(e, "memset(ghost flags)");
         const int grid_ctas = (int)std::min<long long>((long long)sms * occ, p.tasks);
-        if (inter) kern_i<<<grid_ctas, C::NT, C::SMEM_BYTES, st>>>(lmap, smap, p);
-        else kern_n<<<grid_ctas, C::NT, C::SMEM_BYTES, st>>>(lmap, smap, p);
+        if (inter) kern_i<<<grid_ctas, C::NT, C::SMEM_BYTES, st>>>(maps, p);
+        else kern_n<<<grid_ctas, C::NT, C::SMEM_BYTES, st>>>(maps, p);
         if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "gs launch");
         if ((e = cudaEventRecord(S.last, st)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
         done += n;
     }
     return SB_OK;
+}
+
+// One grid (sb_gs): a launch of one slab without neighbours.
+template <class C>
+static int gs_launch(double* grid, int ni, int nj, int nk, int64_t iters, double b, bool inter,
+                     cudaStream_t st, int64_t pitch = 0) {
+    GsLaunchSlab one;
+    one.grid = grid;
+    one.nk = nk;
+    return gs_launch_slabs<C>(&one, 1, {(nk + C::BK - 1) / C::BK}, {0}, ni, nj, iters, b, inter, st,
+                              pitch, gs_window(), false);
 }
 
 int gs_serial_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,
@@ -823,6 +1031,137 @@ int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int ke
     if (v == 1 || (v == 0 && iters <= 2))
         return gs_launch<GsC1>(grid, ni, nj, nk, iters, b, inter, st);
     return gs_launch<GsC>(grid, ni, nj, nk, iters, b, inter, st);
+}
+
+// The cross-GPU z-pipeline in one persistent launch per device
+// (sb_gs_slabs): slab g (grids[g] on devices[g], local planes 0 and nk_g+1
+// are ghost planes) pushes its edge planes' chunks into its neighbours'
+// ghost planes as it stores them and releases their ghost flags, so sweep s
+// of slab g runs behind slab g-1's sweep s and slab g+1's sweep s-1 at chunk
+// granularity (wavefront_order keys are global, so the launches cannot
+// deadlock).  Slabs sharing a device form one launch on streams[first of
+// them].  Returns SB_ERR_PLAN when the layout is not eligible (odd ni,
+// unaligned grids, more than kGsMaxSlabs slabs on one device): the caller
+// then runs the launch-per-sweep pipeline.
+int gs_slabs_fused(int nslabs, const int* devices, double* const* grids, const int64_t* nks, int ni,
+                   int nj, int64_t iters, double b, int kernel, void* const* streams) {
+    using C = GsC;
+    if (ni % 2) return SB_ERR_PLAN;
+    for (int g = 0; g < nslabs; ++g)
+        if (!tma_ok(grids[g], ni)) return SB_ERR_PLAN;
+    // launch groups: slabs per device, in z order
+    std::vector<int> devs;
+    std::vector<std::vector<int>> members;
+    for (int g = 0; g < nslabs; ++g) {
+        auto it = std::find(devs.begin(), devs.end(), devices[g]);
+        if (it == devs.end()) {
+            devs.push_back(devices[g]);
+            members.push_back({g});
+        } else {
+            members[it - devs.begin()].push_back(g);
+        }
+    }
+    for (auto& m : members)
+        if ((int)m.size() > kGsMaxSlabs) return SB_ERR_PLAN;
+    const int tiles_j = (nj + C::BJ - 1) / C::BJ;
+    const size_t gbytes = size_t(C::R) * tiles_j * sizeof(int);
+    std::vector<int> kt(nslabs);
+    for (int g = 0; g < nslabs; ++g) kt[g] = int((nks[g] + C::BK - 1) / C::BK);
+    // ghost flags: [R][tiles_j] per inner side, in the slab's own memory
+    std::vector<int*> glo(nslabs, nullptr), ghi(nslabs, nullptr);
+    cudaError_t e = cudaSuccess;
+    int rc = SB_OK;
+    auto release = [&]() {
+        for (int g = 0; g < nslabs; ++g) {
+            cudaSetDevice(devices[g]);
+            if (glo[g]) cudaFree(glo[g]);
+            if (ghi[g]) cudaFree(ghi[g]);
+        }
+    };
+    for (int g = 0; g < nslabs && rc == SB_OK; ++g) {
+        if ((e = cudaSetDevice(devices[g])) != cudaSuccess) rc = cuda_fail(e, "cudaSetDevice");
+        else if (g > 0 && (e = cudaMalloc(&glo[g], gbytes)) != cudaSuccess) rc = cuda_fail(e, "cudaMalloc");
+        else if (g + 1 < nslabs && (e = cudaMalloc(&ghi[g], gbytes)) != cudaSuccess)
+            rc = cuda_fail(e, "cudaMalloc");
+    }
+    if (rc) {
+        release();
+        return rc;
+    }
+    const int64_t plane = int64_t(ni + 2) * (nj + 2);
+    std::vector<std::vector<GsLaunchSlab>> ls(devs.size());
+    std::vector<std::vector<int>> mine(devs.size(), std::vector<int>(nslabs, -1));
+    for (size_t d = 0; d < devs.size(); ++d)
+        for (size_t i = 0; i < members[d].size(); ++i) {
+            const int g = members[d][i];
+            GsLaunchSlab x;
+            x.grid = grids[g];
+            x.nk = int(nks[g]);
+            x.ghost_lo = glo[g];
+            x.ghost_hi = ghi[g];
+            if (g > 0) {
+                x.push_lo = grids[g - 1] + (nks[g - 1] + 1) * plane;  // below: its plane nk+1
+                x.push_lo_flag = ghi[g - 1];
+                x.lo_remote = devices[g - 1] != devices[g];
+            }
+            if (g + 1 < nslabs) {
+                x.push_hi = grids[g + 1];  // above: its plane 0
+                x.push_hi_flag = glo[g + 1];
+                x.hi_remote = devices[g + 1] != devices[g];
+            }
+            ls[d].push_back(x);
+            mine[d][g] = int(i);
+        }
+    const bool inter = kernel == SB_KERNEL_GS_INTERLEAVED;
+    // one device: one launch, the single-grid schedule; several: a wider
+    // sweep window so that every GPU of the pipeline has work in flight
+    const int window = devs.size() == 1 ? gs_window() : gs_window() * int(devs.size());
+    auto stream_of = [&](size_t d) { return static_cast<cudaStream_t>(streams[members[d][0]]); };
+    if (devs.size() == 1) {
+        cudaSetDevice(devs[0]);
+        rc = gs_launch_slabs<C>(ls[0].data(), (int)ls[0].size(), kt, mine[0], ni, nj, iters, b, inter,
+                                stream_of(0), 0, window, true);
+        if (rc == SB_OK && (e = cudaStreamSynchronize(stream_of(0))) != cudaSuccess)
+            rc = cuda_fail(e, "slab sweeps");
+        if (rc == SB_OK) rc = gs_check_error(stream_of(0));
+    } else {
+        int64_t ntiles_max = 0;
+        for (size_t d = 0; d < devs.size(); ++d) {
+            int64_t n = 0;
+            for (int g : members[d]) n += int64_t(kt[g]) * tiles_j;
+            ntiles_max = std::max(ntiles_max, n);
+        }
+        const int64_t batch = gs_batch_limit<C>(ni, ntiles_max);
+        for (int64_t done = 0; done < iters && rc == SB_OK;) {
+            const int64_t n = std::min(batch, iters - done);
+            // every device's ghost flags are zero before any launch of the batch starts
+            for (size_t d = 0; d < devs.size() && rc == SB_OK; ++d) {
+                cudaSetDevice(devs[d]);
+                for (int g : members[d])
+                    for (int* gf : {glo[g], ghi[g]})
+                        if (gf && (e = cudaMemsetAsync(gf, 0, gbytes, stream_of(d))) != cudaSuccess)
+                            rc = cuda_fail(e, "memset(ghost flags)");
+            }
+            for (size_t d = 0; d < devs.size() && rc == SB_OK; ++d) {
+                cudaSetDevice(devs[d]);
+                if ((e = cudaStreamSynchronize(stream_of(d))) != cudaSuccess) rc = cuda_fail(e, "sync");
+            }
+            for (size_t d = 0; d < devs.size() && rc == SB_OK; ++d) {
+                cudaSetDevice(devs[d]);
+                rc = gs_launch_slabs<C>(ls[d].data(), (int)ls[d].size(), kt, mine[d], ni, nj, n, b, inter,
+                                        stream_of(d), 0, window, false);
+            }
+            for (size_t d = 0; d < devs.size(); ++d) {  // all launches end before the next batch
+                cudaSetDevice(devs[d]);
+                if ((e = cudaStreamSynchronize(stream_of(d))) != cudaSuccess && rc == SB_OK)
+                    rc = cuda_fail(e, "slab sweeps");
+                if (rc == SB_OK) rc = gs_check_error(stream_of(d));
+            }
+            done += n;
+        }
+    }
+    release();
+    return rc;
 }
 
 int gs_serial_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,

@@ -498,6 +498,12 @@ int sb_gs_slabs(int nslabs, const int* devices, double* const* slabs, int64_t ni
     const int64_t plane = (ni + 2) * (nj + 2);
     const size_t pbytes = size_t(plane) * sizeof(double);
     cudaError_t e;
+    // slabs sharing a device share its stream (one launch per device)
+    for (int g = 0; g < nslabs; ++g)
+        for (int h = 0; h < g; ++h)
+            if (S[h].dev == S[g].dev && S[h].st != S[g].st)
+                return fail(SB_ERR_ARGUMENT, "slabs %d and %d share device %d but not a stream", h, g,
+                            S[g].dev);
     for (int g = 0; g < nslabs; ++g) {
         if ((e = cudaSetDevice(S[g].dev)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
         for (int h : {g - 1, g + 1})
@@ -510,6 +516,25 @@ int sb_gs_slabs(int nslabs, const int* devices, double* const* slabs, int64_t ni
                     else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
                 }
             }
+    }
+    // the fused pipeline: one persistent launch per device, edge-plane chunks
+    // pushed into the neighbours' ghost planes as they are stored
+    {
+        std::vector<int64_t> nks(nslabs);
+        std::vector<double*> grids(nslabs);
+        for (int g = 0; g < nslabs; ++g) {
+            nks[g] = S[g].nkl;
+            grids[g] = S[g].g;
+        }
+        rc = gs_slabs_fused(nslabs, devices, grids.data(), nks.data(), (int)ni, (int)nj, iters, b, kernel,
+                            streams);
+        if (rc != SB_ERR_PLAN) return rc;
+        clear_error();
+    }
+    // not eligible (odd ni, unaligned slabs, > 8 slabs on a device): one
+    // sb_gs launch per slab and sweep, ghost planes copied between them
+    for (int g = 0; g < nslabs; ++g) {
+        cudaSetDevice(S[g].dev);
         for (cudaEvent_t* ev : {&S[g].done, &S[g].got_lo, &S[g].got_hi})
             if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
                 return cuda_fail(e, "cudaEventCreate");

@@ -60,6 +60,9 @@ int jacobi_generic_sweep(const double* src, double* dst, int ni, int nj, int nk,
                          cudaStream_t st);
 int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int kernel,
            cudaStream_t st);
+int gs_slabs_fused(int nslabs, const int* devices, double* const* grids, const int64_t* nks, int ni,
+                   int nj, int64_t iters, double b, int kernel, void* const* streams);
+int gs_check_error(cudaStream_t st);
 
 // work schedules of the temporally blocked Jacobi launch (sched.cu)
 int64_t schedule_span(int T, int tiles, int nkout, int grid, int kb);

@@ -298,3 +298,67 @@ def test_c_abi_gs_slabs_full_size(nslabs):
     for s in range(nslabs):
         lo, hi = gs_slab_layout(n, nslabs, s)
         assert torch.equal(bufs[s][1:-1], whole[lo:hi]), s
+
+
+def _gs_slabs_run(g, nslabs, iters, kernel, streams=None):
+    import ctypes
+
+    import torch
+
+    from paper_1004_1741_b200 import _lib
+    from paper_1004_1741_b200.slabs import gs_slab_layout
+
+    lib = _lib.load()
+    bufs = []
+    for s in range(nslabs):
+        lo, hi = gs_slab_layout(g.nk, nslabs, s)
+        bufs.append(torch.from_numpy(np.ascontiguousarray(g.data[lo - 1:hi + 1])).cuda())
+    st = torch.cuda.Stream()
+    devs = (ctypes.c_int * nslabs)(*([0] * nslabs))
+    pa = (ctypes.c_void_p * nslabs)(*[t.data_ptr() for t in bufs])
+    ps = (ctypes.c_void_p * nslabs)(*(streams or [st.cuda_stream] * nslabs))
+    _lib.check(lib.sb_gs_slabs(nslabs, devs, pa, g.ni, g.nj, g.nk, iters, 1 / 6,
+                               _lib.KERNEL_IDS[kernel], ps))
+    return np.concatenate([t[1:-1].cpu().numpy() for t in bufs])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,nslabs,iters,kernel", [
+    ((40, 33, 10), 4, 9, "gs-naive"),          # slabs of 3, 3, 2, 2 planes: one partial tile each
+    ((64, 17, 23), 3, 11, "gs-interleaved"),   # 8, 8, 7 planes; > 3 sweep windows
+    ((39, 20, 18), 2, 5, "gs-naive"),          # odd ni: the launch-per-sweep fallback
+    ((130, 70, 61), 8, 4, "gs-interleaved"),   # 8 slabs in one launch
+])
+def test_gs_fused_slabs_edge_cases(shape, nslabs, iters, kernel):
+    """The fused z-pipeline (one launch for the slabs of a GPU, edge-plane
+    chunks pushed into the neighbours' ghost planes) == the serial sweep."""
+    spec = {"shape": list(shape), "pattern": "random", "seed": 21, "lo": -1.0, "hi": 1.0}
+    g = make_input(spec)
+    want = oracle.run_serial(kernel, g.data, iters, 0.0, 1 / 6)
+    assert sha(_gs_slabs_run(g, nslabs, iters, kernel)) == sha(want[1:-1])
+
+
+@pytest.mark.gpu
+def test_gs_slabs_sharing_a_device_need_one_stream():
+    import torch
+
+    g = make_input({"shape": [16, 8, 8], "pattern": "random", "seed": 1, "lo": 0.0, "hi": 1.0})
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with pytest.raises(ValueError):
+        _gs_slabs_run(g, 2, 1, "gs-naive", streams=[s1.cuda_stream, s2.cuda_stream])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nslabs", [2, 8])
+def test_config5_gs_slabs_vs_reference_hash(hashed_cases, nslabs):
+    """BASELINE config 5 (512^3, U[-1,1), 100 sweeps) as the z-pipeline of
+    `nslabs` slabs == the reference's own result."""
+    from conftest import coeffs_of
+
+    rec = hashed_cases["cfg5_gsn512_mixed_it100"]
+    assert coeffs_of(rec)[1] == 1 / 6
+    g = make_input(rec["spec"])
+    got = _gs_slabs_run(g, nslabs, rec["iters"], rec["kernel"])
+    full = g.data.copy()
+    full[1:-1] = got
+    assert sha(full) == rec["output_sha256"]
