@@ -79,3 +79,33 @@ def test_no_device_is_an_error_not_a_fallback(binding):
         pytest.skip("a GPU is present")
     with pytest.raises(StencilError):
         binding(_plan(variant="wavefront", t=4), _grid(8, 6, 5))
+
+
+@pytest.fixture(scope="module")
+def multi_binding(binding):
+    """INTEGRATION.md section 4's run_b200_multi, executed on top of the
+    section 2 namespace (it reuses _lib, _KID and _EXC)."""
+    text = (ROOT / "INTEGRATION.md").read_text()
+    sec = text[text.index("## 2. Reference-side binding"):]
+    code2 = re.search(r"```python\n(.*?)```", sec, flags=re.S).group(1)
+    code2 = code2.replace("from ..errors import DimensionError, PlanError, PartitionError, "
+                          "ConfigError, StencilError\n", "")
+    code2 = code2.replace('"/path/to/libsb200.so"', repr(str(_lib.LIB_PATH)))
+    sec4 = text[text.index("## 4. Multi-GPU"):]
+    code4 = re.search(r"```python\n(.*?)```", sec4, flags=re.S).group(1)
+    ns = {"DimensionError": DimensionError, "PlanError": PlanError,
+          "PartitionError": PartitionError, "ConfigError": ConfigError,
+          "StencilError": StencilError}
+    exec(compile(code2 + "\n" + code4, "INTEGRATION.md", "exec"), ns)  # noqa: S102
+    return ns["run_b200_multi"]
+
+
+def test_multi_binding_errors_before_any_work(multi_binding):
+    g = _grid(4, 4, 3)
+    assert multi_binding(_plan(iters=0), g, [0, 0]) is g
+    with pytest.raises(PartitionError):  # more GPUs than planes
+        multi_binding(_plan(), g, [0, 0, 0, 0])
+    with pytest.raises(DimensionError):
+        multi_binding(_plan(), _grid(0, 4, 4), [0])
+    with pytest.raises(PlanError):
+        multi_binding(_plan(iters=-2), g, [0])
