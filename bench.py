@@ -464,6 +464,27 @@ def run_gpu_arm(args):
                 "single_sweep_roofline_mlups": PEAKS["hbm_gbs"] * 1e9 / 16 / 1e6,
                 "x_single_sweep_roofline": value / world / (PEAKS["hbm_gbs"] * 1e9 / 16 / 1e6)}
 
+    # secondary (compute) ceiling: the FP64 pipe.  sb_fp64_probe measures the
+    # device's sustained DP operation rate; the kernel needs 7 DP operations
+    # per useful LUP at a = 0 (5 adds, b*acc, the fused a*c + ...), and the
+    # overlapped tiles execute (64 x 32) / (TO x TJ) times that (trapezoid).
+    fp64 = None
+    try:
+        from paper_1004_1741_b200.perf import fp64_peak
+
+        peak_ops = fp64_peak(device=local)
+        _, dims = _lib.jacobi_schedule(depth, NI, NJ, 1, NK_PER_GPU + 1, 148)
+        overlap = (64 * 32) / (dims[0] * dims[1]) if depth == 4 else None
+        useful = 7.0 * SWEEPS * cells_per_gpu * args.steps / sec  # per GPU
+        fp64 = {"bound": "fp64", "peak_dp_ops_per_s": peak_ops, "dp_ops_per_lup": 7,
+                "achieved_dp_ops_per_s": useful, "frac": useful / peak_ops,
+                "executed_overlap_factor": overlap,
+                "executed_frac": useful * overlap / peak_ops if overlap else None,
+                "peak_source": "sb_fp64_probe (independent DADD chains on every SM, this run)"}
+    except Exception as exc:  # noqa: BLE001 -- a diagnostic; never fails the bench
+        fp64 = {"error": str(exc)}
+    roofline["fp64"] = fp64
+
     # e2e through the public C-ABI host-buffer entry point: every step one
     # grid goes pinned host -> H2D -> SWEEPS sweeps -> D2H.  At N=1 the steps
     # go through sb_run_host_batch, which overlaps step i's upload with step

@@ -203,6 +203,16 @@ int sb_run_host_batch(int kernel, double* const* host_grids, int count, int64_t 
 int sb_triad(double* a, const double* b, const double* c, double s, int64_t n, void* stream);
 
 /*
+ * FP64 pipe probe: one launch of independent double-precision add chains
+ * (no memory traffic) filling every SM; *ops receives the number of DP
+ * operations it executes, so ops / elapsed time is the device's sustained
+ * FP64 issue rate -- the secondary (compute) ceiling of the stencil kernels
+ * (SURVEY.md 8(d)).  `sink` is a device buffer of >= 256 doubles (written
+ * only to keep the chains alive).  Asynchronous on `stream`.
+ */
+int sb_fp64_probe(double* sink, int64_t iters, void* stream, int64_t* ops);
+
+/*
  * Frees the device buffers the library keeps between calls on `device` (all
  * devices if < 0): the host-entry slots of sb_run_host / sb_run_host_batch
  * (the batch holds up to six grids' worth) and the pitched copies used for

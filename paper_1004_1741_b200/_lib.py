@@ -51,6 +51,7 @@ SIGNATURES = {
     "sb_run_host": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _dbl, _dbl, _int, _int]),
     "sb_run_host_batch": (_int, [_int, _vp, _int, _i64, _i64, _i64, _i64, _dbl, _dbl, _int, _int]),
     "sb_triad": (_int, [_vp, _vp, _vp, _dbl, _i64, _vp]),
+    "sb_fp64_probe": (_int, [_vp, _i64, _vp, ctypes.POINTER(_i64)]),
     "sb_host_alloc": (_vp, [_i64]),
     "sb_release_caches": (_int, [_int]),
     "sb_host_free": (None, [_vp]),

@@ -233,6 +233,26 @@ __global__ void triad_kernel(double* __restrict__ a, const double* __restrict__ 
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) a[n - 1] = __dadd_rn(b[n - 1], __dmul_rn(s, c[n - 1]));
 }
 
+// FP64 pipe probe: kFp64Chains independent DADD chains per thread, no memory
+// traffic in the loop.  With the SMs full of warps this runs at the FP64
+// pipe's issue limit: the secondary ceiling of the stencil kernels (SURVEY
+// 8(d): "fp64 pipe ... measure on the box").
+constexpr int kFp64Chains = 8;
+__global__ void fp64_probe_kernel(double* sink, int64_t iters) {
+    double x[kFp64Chains];
+#pragma unroll
+    for (int c = 0; c < kFp64Chains; ++c) x[c] = 1.0 + 1e-3 * (threadIdx.x + c);
+    const double d = 1e-300 * (1 + blockIdx.x % 3);
+    for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int c = 0; c < kFp64Chains; ++c) x[c] = __dadd_rn(x[c], d);
+    }
+    double acc = 0;
+#pragma unroll
+    for (int c = 0; c < kFp64Chains; ++c) acc = __dadd_rn(acc, x[c]);
+    if (acc == 12345.0) sink[threadIdx.x] = acc;  // keeps the chains alive
+}
+
 // ---------------------------------------------------------------------------
 // temporally blocked launch
 
@@ -671,6 +691,21 @@ int sb_triad(double* a, const double* b, const double* c, double s, int64_t n, v
     triad_kernel<<<sms * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, b, c, s, n);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? SB_OK : cuda_fail(e, "triad launch");
+}
+
+int sb_fp64_probe(double* sink, int64_t iters, void* stream, int64_t* ops) {
+    clear_error();
+    if (!sink || !ops || iters < 1) return fail(SB_ERR_ARGUMENT, "need a sink, an op counter and iters >= 1");
+    int dev = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "device query");
+    const int blocks = sms * 8, threads = 256;  // 64 warps per SM
+    fp64_probe_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(sink, iters);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "fp64 probe launch");
+    *ops = int64_t(blocks) * threads * iters * kFp64Chains;
+    return SB_OK;
 }
 
 double* sb_host_alloc(int64_t count) {

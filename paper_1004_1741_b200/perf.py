@@ -151,6 +151,36 @@ def stream_triad(elements=1 << 28, repetitions=5, warmup=1, device=0):
                         validated=validated, device=device)
 
 
+def fp64_peak(iters=1 << 16, repetitions=3, device=0):
+    """Sustained FP64 operation rate of the device (sb_fp64_probe:
+    independent DADD chains on every SM, CUDA-event timed, best of
+    `repetitions`), in DP operations per second -- the compute ceiling the
+    stencil kernels are measured against besides HBM bandwidth."""
+    import torch
+
+    from . import _lib
+
+    _lib.require_device()
+    lib = _lib.load()
+    dev = torch.device("cuda", device)
+    sink = torch.zeros(256, dtype=torch.float64, device=dev)
+    ops = ctypes.c_int64(0)
+    best = None
+    with torch.cuda.device(dev):
+        st = torch.cuda.current_stream()
+        sp = ctypes.c_void_p(st.cuda_stream)
+        _lib.check(lib.sb_fp64_probe(sink.data_ptr(), 256, sp, ctypes.byref(ops)))  # warm-up
+        for _ in range(repetitions):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            _lib.check(lib.sb_fp64_probe(sink.data_ptr(), iters, sp, ctypes.byref(ops)))
+            e1.record(st)
+            _lib.check(lib.sb_sync(sp))
+            sec = e0.elapsed_time(e1) / 1e3
+            best = sec if best is None else min(best, sec)
+    return ops.value / best
+
+
 @dataclass
 class Measurement:
     kernel: str

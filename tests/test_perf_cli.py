@@ -86,3 +86,13 @@ def test_cli_gpus_threaded_and_pipeline(capsys, tmp_path):
 
 def test_cli_gpus_argument_errors(capsys):
     assert main(["verify", "--kernel", "jacobi", "--variant", "threaded", "--gpus", "0"]) == 2
+
+
+@pytest.mark.gpu
+def test_fp64_probe_rate_is_plausible():
+    """sb_fp64_probe: B200 FP64 is ~37 TFLOP/s counting an FMA as 2, i.e.
+    ~18 T DP operations/s at boost clock; the probe must land near that."""
+    from paper_1004_1741_b200.perf import fp64_peak
+
+    ops = fp64_peak(iters=1 << 14)
+    assert 8e12 < ops < 30e12, ops
