@@ -489,3 +489,28 @@ def test_gs_full_size_schedule_independent(kernel):
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
     del outs
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("shape,iters", [
+    ((4096, 2050, 3), 4),      # wide planes, one tile-row more than a multiple, 3 planes
+    ((2, 2, 100000), 5),       # one tile, 100k planes (long items, k-pieces)
+    ((1, 3, 20000), 3),        # ni = 1: pitched / serial fallbacks
+    ((16384, 7, 5), 2),        # 16k-wide rows, ragged j
+])
+def test_extreme_aspect_ratios_vs_oracle(shape, iters):
+    """Extents at the edges of the tilings (many tiles in one direction, a
+    single tile in another, deep k with tiny planes) == the oracle, for the
+    fused Jacobi (depths 1, 3, 4), both GS associations, and -- for Jacobi
+    -- a 2-slab run through the drop-in."""
+    ni, nj, nk = shape
+    data = make_input({"shape": [ni, nj, nk], "pattern": "random", "seed": 99, "lo": -1.0,
+                       "hi": 1.0}).data
+    want = oracle.run_serial("jacobi", data, 4, 0.5, 0.1)
+    for depth in (1, 3, 4):
+        assert sha(run_device("jacobi", data, 4, 0.5, 0.1, depth)) == sha(want), (shape, depth)
+    g = Grid3D(ni, nj, nk, np.array(data))
+    out = run(SweepPlan("jacobi", "threaded", 4, coeffs=StencilCoeffs(0.5, 0.1)), g, devices=[0, 0])
+    assert sha(out.data) == sha(want), shape
+    for kern in ("gs-naive", "gs-interleaved"):
+        want = oracle.run_serial(kern, data, iters, 0.0, 1 / 6)
+        assert sha(run_device(kern, data, iters, 0.0, 1 / 6, 1)) == sha(want), (shape, kern)
