@@ -22,10 +22,9 @@
 
 #include "../../include/stencil_b200.h"
 #include "sb_internal.h"
+#include "jacobi_tb.cuh"
 
 namespace sb {
-int jacobi_block(const double* src, double* dst, int ni, int nj, int nk, int kfirst, int klast,
-                 int T, double a, double b, cudaStream_t st);
 int gs_check_error(cudaStream_t st);
 
 // cached device buffers + stream per device for sb_run_host
@@ -372,6 +371,83 @@ int sb_jacobi_slabs(int nslabs, const int* devices, double* const* slabs, double
         if ((rc = halo_copy(S[s].buf[0], S[s].buf[1], (int)ni, (int)nj, (int)S[s].nkl, S[s].st))) return rc;
     }
     int cur = 0;  // buffer index holding the current field
+    // Fused exchange (every slab TMA-addressable): per slab and period, the
+    // `depth` edge planes on each inner side are computed first by launches
+    // whose threads also write them into the neighbours' ghost planes (peer
+    // memory over NVLink between GPUs; JacPeers) -- no separate copies -- then
+    // the interior by the plain kernel.  Period p of slab s waits for period
+    // p-1 of s-1 and s+1: its ghosts were written there, and they read the
+    // planes this period's edge launches overwrite.  Events alternate by
+    // period parity so that a wait never lands on the same period.
+    bool fused = (ni % 2 == 0);
+    for (int s = 0; s < nslabs; ++s)
+        fused = fused && tma_ok(S[s].buf[0], ni) && tma_ok(S[s].buf[1], ni);
+    if (fused) {
+        std::vector<cudaEvent_t> pev[2];
+        for (int par = 0; par < 2; ++par) {
+            pev[par].assign(nslabs, nullptr);
+            for (int s = 0; s < nslabs; ++s) {
+                cudaSetDevice(S[s].dev);
+                if ((e = cudaEventCreateWithFlags(&pev[par][s], cudaEventDisableTiming)) != cudaSuccess)
+                    return cuda_fail(e, "cudaEventCreate");
+            }
+        }
+        rc = SB_OK;
+        int64_t period = 0;
+        for (int64_t done = 0; done < iters && rc == SB_OK; ++period) {
+            const int T = (int)std::min<int64_t>(depth, iters - done);
+            const int par = int(period & 1);
+            for (int s = 0; s < nslabs && rc == SB_OK; ++s) {
+                Slab& X = S[s];
+                cudaSetDevice(X.dev);
+                if (period > 0) {
+                    if (s > 0) cudaStreamWaitEvent(X.st, pev[par ^ 1][s - 1], 0);
+                    if (s + 1 < nslabs) cudaStreamWaitEvent(X.st, pev[par ^ 1][s + 1], 0);
+                }
+                const int64_t lo = X.glo, hi = X.glo + (X.own_hi - X.own_lo);  // owned, local padded
+                JacPeers pe;
+                memset(&pe, 0, sizeof pe);
+                if (s + 1 < nslabs) {  // top `depth` owned planes -> the slab above's planes [0, depth)
+                    pe.buf[0] = S[s + 1].buf[cur ^ 1];
+                    pe.k0[0] = int(hi - depth);
+                    pe.k1[0] = int(hi);
+                    pe.off[0] = int(depth - hi);
+                }
+                if (s > 0) {  // bottom `depth` owned planes -> the slab below's [Y.hi, Y.hi + depth)
+                    const Slab& Y = S[s - 1];
+                    pe.buf[1] = Y.buf[cur ^ 1];
+                    pe.k0[1] = int(lo);
+                    pe.k1[1] = int(lo + depth);
+                    pe.off[1] = int(Y.glo + (Y.own_hi - Y.own_lo) - lo);
+                }
+                const JacPeers* pp = (pe.buf[0] || pe.buf[1]) ? &pe : nullptr;
+                const int64_t elo = (s > 0) ? std::min<int64_t>(lo + depth, hi) : lo;
+                const int64_t ehi = (s + 1 < nslabs) ? std::max<int64_t>(hi - depth, elo) : hi;
+                const double* src = X.buf[cur];
+                double* dst = X.buf[cur ^ 1];
+                const int nkl = (int)X.nkl;
+                if (elo > lo)
+                    rc = jacobi_block(src, dst, (int)ni, (int)nj, nkl, (int)lo, (int)elo, T, a, b, X.st, pp);
+                if (rc == SB_OK && hi > ehi)
+                    rc = jacobi_block(src, dst, (int)ni, (int)nj, nkl, (int)ehi, (int)hi, T, a, b, X.st, pp);
+                if (rc == SB_OK && ehi > elo)
+                    rc = jacobi_block(src, dst, (int)ni, (int)nj, nkl, (int)elo, (int)ehi, T, a, b, X.st);
+                if (rc == SB_OK) cudaEventRecord(pev[par][s], X.st);
+            }
+            cur ^= 1;
+            done += T;
+        }
+        for (int s = 0; s < nslabs; ++s) {
+            cudaSetDevice(S[s].dev);
+            if ((e = cudaStreamSynchronize(S[s].st)) != cudaSuccess && rc == SB_OK)
+                rc = cuda_fail(e, "slab sweeps");
+            cudaStreamDestroy(S[s].comm);
+            for (cudaEvent_t ev : {S[s].edge, S[s].start, S[s].sent_up, S[s].sent_dn}) cudaEventDestroy(ev);
+            for (int par = 0; par < 2; ++par) cudaEventDestroy(pev[par][s]);
+        }
+        *result_in_scratch = cur;
+        return rc;
+    }
     bool first = true;
     for (int64_t done = 0; done < iters;) {
         const int T = (int)std::min<int64_t>(depth, iters - done);

@@ -53,6 +53,18 @@
 
 namespace sb {
 
+// Halo planes sent straight from a slab launch into its neighbours' ghost
+// planes (the fused z-slab exchange, sb_jacobi_slabs): output plane k in
+// [k0[q], k1[q]) is also written, by the threads that computed it, to plane
+// k + off[q] of buf[q] -- a buffer of the same plane shape on the
+// neighbouring slab (peer memory over NVLink when that slab is on another
+// GPU).  buf[q] == nullptr: no neighbour on that side.
+struct JacPeers {
+    double* buf[2];
+    int k0[2], k1[2];
+    int off[2];
+};
+
 struct JacobiParams {
     int ni, nj, nk;          // interior extents
     int kfirst, klast;       // output planes [kfirst, klast) (padded indices, within [1, nk])
@@ -66,6 +78,7 @@ struct JacobiParams {
     int* counter;            // work counter (zeroed before launch)
     double* dst;             // output grid
     int64_t plane;           // (nj + 2) * (ni + 2) cells, < 2^31 (check_dims)
+    JacPeers peers;          // fused halo exchange (zero: none)
 };
 
 template <int T_, int RJ_, int NW_, int S_, int MINB_, bool L1S_ = false, bool TS_ = false,
@@ -162,6 +175,30 @@ __device__ __forceinline__ ItemInfo decode_item(const JacobiParams& p, int item)
 __device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void sts2(double* p, double x, double y) {
     *reinterpret_cast<double2*>(p) = make_double2(x, y);
+}
+
+// Fused halo exchange (JacobiParams::peers; kernels instantiated with PEER,
+// used for a slab's edge-plane launches only): output plane k, staged in
+// shared memory as the TO x TJ tile at (I0, J0), is copied by the whole CTA
+// into the neighbour slab's ghost plane (peer memory over NVLink between
+// GPUs).  The staging buffer is next overwritten two steps later, after
+// another barrier.
+template <class C>
+__device__ __forceinline__ void peer_copy(const JacobiParams& p, const double* stg, int I0, int J0,
+                                          int k) {
+    constexpr int PAIRS = C::TO / 2;
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+        if (!p.peers.buf[q] || k < p.peers.k0[q] || k >= p.peers.k1[q]) continue;
+        double* plane = p.peers.buf[q] + (int64_t)(k + p.peers.off[q]) * p.plane;
+        for (int x = threadIdx.x; x < C::TJ * PAIRS; x += C::NT) {
+            const int row = x / PAIRS, i2 = 2 * (x - row * PAIRS);
+            const int gj = J0 + row, gi = I0 + i2;
+            if (gj <= p.nj && gi <= p.ni)  // inside the grid (gi + 1 <= ni + 1)
+                *reinterpret_cast<double2*>(plane + (int64_t)gj * (p.ni + 2) + gi) =
+                    lds2(stg + row * C::TO + i2);
+        }
+    }
 }
 
 // Per-thread state of one level's input: three plane slots rotating with
@@ -393,7 +430,7 @@ __device__ __forceinline__ void level_finish(const double (&cc)[C::RJ][2],
 // which nothing else needs.  Phase 2 is the short dependent chain through the
 // levels: level L's new plane is level L+1's U.  (SEL/SLOW steps keep the
 // one-pass form: their masks made the two-phase code longer than it gained.)
-template <class C, int MODE, bool AZ, int PH>
+template <class C, int MODE, bool AZ, int PH, bool PEER>
 __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CUtensorMap* dst_map,
                                             const JacobiParams& p,
                                             double* ring, double* xb, uint64_t* full,
@@ -588,6 +625,15 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
         if (tid == 0) bulk_wait_read<0>();
     }
     __syncthreads();
+    // fused halo exchange: an edge output plane, staged in shared memory, is
+    // also copied by the whole CTA into the neighbour slab's ghost plane
+    // (CTA-uniform; only the `depth` edge planes of a slab launch).  The
+    // staging buffer is next overwritten two steps later, after another
+    // barrier.
+    if constexpr (PEER) {
+        if (out_step) peer_copy<C>(p, ring + C::STG_OFF + (s.g & 1) * C::STG, it.I0, it.J0,
+                                   it.kb - 2 * T + s.n);
+    }
     if (tid == 0) {
         if (C::TS && out_step) {
             tma_store_3d(dst_map, ring + C::STG_OFF + (s.g & 1) * C::STG, it.I0, it.J0,
@@ -607,7 +653,7 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
 
 // `count` plane steps of the current item (all in one StepMode),
 // entering the 3-phase register rotation at g mod 3.
-template <class C, int MODE, bool AZ>
+template <class C, int MODE, bool AZ, bool PEER>
 __device__ __forceinline__ void jacobi_steps(const CUtensorMap* src_map, const CUtensorMap* dst_map,
                                              const JacobiParams& p,
                                              double* ring, double* xb, uint64_t* full,
@@ -616,25 +662,25 @@ __device__ __forceinline__ void jacobi_steps(const CUtensorMap* src_map, const C
     if (count <= 0) return;
     const int ph = s.g % 3;
     if (ph == 1) {
-        jacobi_step<C, MODE, AZ, 1>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 1, PEER>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
-        jacobi_step<C, MODE, AZ, 2>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 2, PEER>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
     } else if (ph == 2) {
-        jacobi_step<C, MODE, AZ, 2>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 2, PEER>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
     }
     while (true) {
-        jacobi_step<C, MODE, AZ, 0>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 0, PEER>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
-        jacobi_step<C, MODE, AZ, 1>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 1, PEER>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
-        jacobi_step<C, MODE, AZ, 2>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
+        jacobi_step<C, MODE, AZ, 2, PEER>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
         if (--count == 0) return;
     }
 }
 
-template <class C, bool AZ>
+template <class C, bool AZ, bool PEER = false>
 __global__ void __launch_bounds__(C::NT, C::MINB)
 jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
                  const __grid_constant__ CUtensorMap dst_map, const JacobiParams p) {
@@ -701,16 +747,16 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
         const int n_lo = min(s.it.N, max(0, 2 * T + 1 - s.it.kb));
         const int n_hi = max(n_lo, min(s.it.N, p.nk + 2 + T - s.it.kb));
         if constexpr (C::UNI) {
-            jacobi_steps<C, MASK, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, s.it.N);
+            jacobi_steps<C, MASK, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, s.it.N);
         } else {
-            jacobi_steps<C, SLOW, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, n_lo);
+            jacobi_steps<C, SLOW, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, n_lo);
             if (ij_in)
-                jacobi_steps<C, FAST, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
+                jacobi_steps<C, FAST, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
                                           n_hi - n_lo);
             else
-                jacobi_steps<C, SEL, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
+                jacobi_steps<C, SEL, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
                                          n_hi - n_lo);
-            jacobi_steps<C, SLOW, AZ>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
+            jacobi_steps<C, SLOW, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
                                       s.it.N - n_hi);
         }
         s.n = 0;

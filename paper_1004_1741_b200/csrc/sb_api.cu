@@ -294,12 +294,14 @@ static TbPlan tb_plan(int ni, int nj, int kfirst, int klast, int grid) {
 
 template <class C, bool AZ>
 static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk, int kfirst,
-                          int klast, double a, double b, cudaStream_t st, int64_t pitch) {
+                          int klast, double a, double b, cudaStream_t st, int64_t pitch,
+                          const JacPeers* peers) {
     int* counters;
     int sms;
     int rc = get_counters(&counters, &sms);
     if (rc) return rc;
-    auto kern = jacobi_tb_kernel<C, AZ>;
+    // the fused-exchange variant only where a launch sends planes
+    auto kern = peers ? jacobi_tb_kernel<C, AZ, true> : jacobi_tb_kernel<C, AZ, false>;
     int per_sm = 0;
     if ((rc = ctas_per_sm((const void*)kern, C::NT, C::SMEM_BYTES, &per_sm))) return rc;
     const int occ = per_sm * sms;  // resident CTAs on the device
@@ -319,6 +321,11 @@ static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk
     p.ni = ni;
     p.nj = nj;
     p.nk = nk;
+    memset(&p.peers, 0, sizeof p.peers);
+    if (peers) {
+        if (!C::TS || pitch != nip) return fail(SB_ERR_PLAN, "fused halo exchange needs a TMA-store depth");
+        p.peers = *peers;
+    }
     const int grid = occ;  // resident CTAs
     const TbPlan pl = tb_plan<C>(ni, nj, kfirst, klast, grid);
     p.tiles_i = pl.tiles_i;
@@ -359,10 +366,11 @@ static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk
 
 template <class C>
 static int launch_tb(const double* src, double* dst, int ni, int nj, int nk, int kfirst, int klast,
-                     double a, double b, cudaStream_t st, int64_t pitch = 0) {
+                     double a, double b, cudaStream_t st, int64_t pitch = 0,
+                     const JacPeers* peers = nullptr) {
     if (a == 0.0)
-        return launch_tb_impl<C, true>(src, dst, ni, nj, nk, kfirst, klast, a, b, st, pitch);
-    return launch_tb_impl<C, false>(src, dst, ni, nj, nk, kfirst, klast, a, b, st, pitch);
+        return launch_tb_impl<C, true>(src, dst, ni, nj, nk, kfirst, klast, a, b, st, pitch, peers);
+    return launch_tb_impl<C, false>(src, dst, ni, nj, nk, kfirst, klast, a, b, st, pitch, peers);
 }
 
 // Tile configurations per depth: <T, RJ rows/thread, NW warps, S ring stages,
@@ -405,8 +413,9 @@ static int with_cfg(int T, F&& f) {
         // per HBM pass" sweep): 12 warps x 2 rows; level 1 reads the TMA
         // ring (L1S), level T stores through TMA (TS), one step loop (UNI) --
         // the register-lean form (ptxas: 0 / 0 / 12 / 952 spill bytes at
-        // T = 5..8; the plain form spilled 0 / 156 / 6364 / 9736)
-        case 5: SB_L(5, 2, 12, 3, 1);
+        // T = 5..8; the plain form spilled 0 / 156 / 6364 / 9736).  Every
+        // depth stores through TMA, which the fused slab exchange relies on.
+        case 5: SB_L(5, 2, 12, 3, 1, true, true);
         case 6: SB_L(6, 2, 12, 3, 1, true, true, true);
         case 7: SB_L(7, 2, 12, 3, 1, true, true, true);
         case 8: SB_L(8, 2, 12, 3, 1, true, true, true);
@@ -416,10 +425,11 @@ static int with_cfg(int T, F&& f) {
 }
 
 static int launch_depth(int T, const double* src, double* dst, int ni, int nj, int nk, int kfirst,
-                        int klast, double a, double b, cudaStream_t st, int64_t pitch = 0) {
+                        int klast, double a, double b, cudaStream_t st, int64_t pitch = 0,
+                        const JacPeers* peers = nullptr) {
     if (klast <= kfirst) return SB_OK;
     return with_cfg(T, [&](auto cfg) {
-        return launch_tb<decltype(cfg)>(src, dst, ni, nj, nk, kfirst, klast, a, b, st, pitch);
+        return launch_tb<decltype(cfg)>(src, dst, ni, nj, nk, kfirst, klast, a, b, st, pitch, peers);
     });
 }
 
@@ -496,7 +506,11 @@ int halo_copy(const double* src, double* dst, int ni, int nj, int nk, cudaStream
 // T fused sweeps src -> dst (T = 1 for grids TMA cannot describe), output
 // planes [kfirst, klast) only.
 int jacobi_block(const double* src, double* dst, int ni, int nj, int nk, int kfirst, int klast,
-                 int T, double a, double b, cudaStream_t st) {
+                 int T, double a, double b, cudaStream_t st, const JacPeers* peers) {
+    if (peers) {  // fused exchange: the TMA path only (the caller checked tma_ok)
+        if (!(tma_ok(src, ni) && tma_ok(dst, ni))) return fail(SB_ERR_PLAN, "fused exchange needs even ni");
+        return launch_depth(T, src, dst, ni, nj, nk, kfirst, klast, a, b, st, 0, peers);
+    }
     if (tma_ok(src, ni) && tma_ok(dst, ni))
         return launch_depth(T, src, dst, ni, nj, nk, kfirst, klast, a, b, st);
     if (T != 1) return fail(SB_ERR_PLAN, "depth %d needs an even ni (16-byte row pitch)", T);

@@ -8,6 +8,8 @@
 
 namespace sb {
 
+struct JacPeers;  // jacobi_tb.cuh
+
 // Tuning knobs (SB_KBLK, SB_LIST*, SB_GS_WINDOW, SB_GSCFG, SB_JCFG) are read
 // from the environment only in experiment builds (-DSB_EXPERIMENTS, tools/);
 // the product library always runs its measured defaults.
@@ -54,6 +56,8 @@ int make_grid_map3p(CUtensorMap* m, const double* base, int64_t nip, int64_t njp
 int get_counters(int** counters, int* sms);
 bool tma_ok(const void* p, int64_t ni);
 int halo_copy(const double* src, double* dst, int ni, int nj, int nk, cudaStream_t st);
+int jacobi_block(const double* src, double* dst, int ni, int nj, int nk, int kfirst, int klast,
+                 int T, double a, double b, cudaStream_t st, const JacPeers* peers = nullptr);
 int jacobi_run(double* a_buf, double* b_buf, int ni, int nj, int nk, int64_t iters, double a,
                double b, int depth, cudaStream_t st, int* in_b);
 int jacobi_generic_sweep(const double* src, double* dst, int ni, int nj, int nk, double a, double b,
