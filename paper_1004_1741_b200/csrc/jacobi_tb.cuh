@@ -85,11 +85,10 @@ template <int T_, int RJ_, int NW_, int S_, int MINB_, bool L1S_ = false, bool T
           bool UNI_ = false>
 struct JacobiCfg {
     static constexpr int T = T_, RJ = RJ_, NW = NW_, S = S_, MINB = MINB_;
-    // UNI: one step loop for every step of an item (StepMode MASK: the FAST
-    // arithmetic, then a per-cell select against Dirichlet masks that also
-    // cover the k-boundary planes) instead of SLOW / FAST|SEL / SLOW loops.
-    // One inlined loop instead of three leaves ptxas room for 5 rows per
-    // thread at T = 4 without spilling.
+    // UNI: every step of an item in StepMode MASK (one inlined step loop)
+    // instead of MASK / FAST-or-MASK / MASK segments: no FAST loop at all.
+    // One loop instead of two leaves ptxas room for 5 rows per thread at
+    // T = 4 without spilling.
     static constexpr bool UNI = UNI_;
     // TS: level T writes its output tile into a shared staging buffer (double
     // buffered) and one thread stores it with a TMA tensor store per plane,
@@ -226,7 +225,7 @@ struct JState {      // per-thread loop state shared by the step functions
     ItemInfo it;     // current item
     uint32_t ooff;   // this thread's output cell (row 0) within a plane
     uint32_t omask;  // bit r: row r of this thread is an output row of the current item
-    uint32_t keep0, keep1;  // bit r: cell 0 / 1 of row r is a Dirichlet cell (SEL steps)
+    uint32_t keep0, keep1;  // bit r: cell 0 / 1 of row r is a Dirichlet cell (MASK steps)
     uint32_t smask;  // TS: bit r: row r of this thread lies in the staged output tile
     int soff;        // TS: staging offset of this thread's row 0
 };
@@ -296,69 +295,16 @@ __device__ __forceinline__ void produce(const CUtensorMap* src_map, const Jacobi
     }
 }
 
-// Step modes.  FAST: every cell the tile computes at this step is interior.
-// SEL: the planes are interior but the tile touches the i/j boundary: the
-// FAST arithmetic, then Dirichlet cells keep their value (per-item masks).
-// SLOW: anything (k-boundary steps, tiny grids): full predication, and rows
-// outside a level's trapezoid skip their arithmetic.  MASK (JacobiCfg::UNI):
-// any step, FAST arithmetic everywhere, then Dirichlet cells -- i/j masks
-// of the item, plus every cell of a level whose plane lies outside [1, nk] --
-// keep their value.  Cells outside a level's trapezoid then hold values that
-// no output depends on (level L+1 reads level L only inside its own,
-// smaller, trapezoid grown by one cell).
-enum StepMode { SLOW = 0, FAST = 1, SEL = 2, MASK = 3 };
-
-// One level's update of a thread's RJ rows x 2 cells in one pass (SEL and
-// SLOW steps).  cen: the centre
-// plane with the south (row 0) and north (row RJ+1) neighbour rows; dn/up:
-// the planes below and above.
-template <class C, int MODE, bool AZ>
-__device__ __forceinline__ void level_update(const double (&cen)[C::RJ + 2][2],
-                                             const double (&dn)[C::RJ][2],
-                                             const double (&up)[C::RJ][2], double (&nv)[C::RJ][2],
-                                             double a, double b, int L, int dj, int k, int gj,
-                                             bool in_i0, bool in_i1, const JacobiParams& p,
-                                             const JState& s) {
-    constexpr int T = C::T, RJ = C::RJ;
-#pragma unroll
-    for (int r = 0; r < RJ; ++r) {
-        const double c0 = cen[r + 1][0], c1 = cen[r + 1][1];
-        const double wv = __shfl_up_sync(0xffffffffu, c1, 1);    // cell i-1 (lane-1)
-        const double ev = __shfl_down_sync(0xffffffffu, c0, 1);  // cell i+2 (lane+1)
-        bool compute = true;
-        if (MODE == SLOW) {
-            const int jr = dj + r, need = T - L;
-            compute = (jr >= -need) && (jr < C::TJ + need) && (k >= 1) && (k <= p.nk) &&
-                      (gj + r >= 1) && (gj + r <= p.nj);
-        }
-        if (compute) {
-            double acc0 = __dadd_rn(wv, c1), acc1 = __dadd_rn(c0, ev);
-            acc0 = __dadd_rn(acc0, cen[r][0]);
-            acc1 = __dadd_rn(acc1, cen[r][1]);
-            acc0 = __dadd_rn(acc0, cen[r + 2][0]);
-            acc1 = __dadd_rn(acc1, cen[r + 2][1]);
-            acc0 = __dadd_rn(acc0, dn[r][0]);
-            acc1 = __dadd_rn(acc1, dn[r][1]);
-            acc0 = __dadd_rn(acc0, up[r][0]);
-            acc1 = __dadd_rn(acc1, up[r][1]);
-            const double o0 = jac_final<AZ>(a, b, c0, acc0);
-            const double o1 = jac_final<AZ>(a, b, c1, acc1);
-            if (MODE == FAST) {
-                nv[r][0] = o0;
-                nv[r][1] = o1;
-            } else if (MODE == SEL) {
-                nv[r][0] = (s.keep0 & (1u << r)) ? c0 : o0;
-                nv[r][1] = (s.keep1 & (1u << r)) ? c1 : o1;
-            } else {
-                nv[r][0] = in_i0 ? o0 : c0;
-                nv[r][1] = in_i1 ? o1 : c1;
-            }
-        } else {
-            nv[r][0] = c0;  // halo rows/planes keep their value; unneeded rows: anything
-            nv[r][1] = c1;
-        }
-    }
-}
+// Step modes.  FAST: every cell the tile computes at this step is interior
+// (no masks).  MASK: any step -- the same two-phase arithmetic everywhere,
+// then Dirichlet cells (the item's i/j masks, plus every cell of a level
+// whose plane lies outside [1, nk]) keep their value.  Cells outside a
+// level's trapezoid then hold values that no output depends on (level L+1
+// reads level L only inside its own, smaller, trapezoid grown by one cell).
+// MASK replaced round 1's one-pass SLOW (full predication; k-boundary steps
+// and tiny grids) and SEL (border tiles): +3% at 512^3 where every whole-k
+// item has 2(2T+1) k-boundary steps (profiles/r2/ab_mask_modes.log).
+enum StepMode { FAST = 1, MASK = 3 };
 
 // Phase 1 of a level: the partial sums P = ((((W+E)+S)+N)+D) of the RJ rows
 // x 2 cells.  cen: the centre plane with the south (row 0) and north (row
@@ -383,15 +329,14 @@ __device__ __forceinline__ void level_partial(const double (&cen)[C::RJ + 2][2],
 }
 
 // Phase 2 of a level: v = a*c + b*(P + U) (the reference association, see
-// jac_final), then the step mode's Dirichlet / trapezoid handling.
+// jac_final), then the step mode's Dirichlet handling (k: the level's plane).
 template <class C, int MODE, bool AZ>
 __device__ __forceinline__ void level_finish(const double (&cc)[C::RJ][2],
                                              const double (&P)[C::RJ][2],
                                              const double (&up)[C::RJ][2], double (&nv)[C::RJ][2],
-                                             double a, double b, int L, int dj, int k, int gj,
-                                             bool in_i0, bool in_i1, const JacobiParams& p,
+                                             double a, double b, int k, const JacobiParams& p,
                                              const JState& s) {
-    constexpr int T = C::T, RJ = C::RJ;
+    constexpr int RJ = C::RJ;
 #pragma unroll
     for (int r = 0; r < RJ; ++r) {
         const double c0 = cc[r][0], c1 = cc[r][1];
@@ -400,20 +345,10 @@ __device__ __forceinline__ void level_finish(const double (&cc)[C::RJ][2],
         if (MODE == FAST) {
             nv[r][0] = o0;
             nv[r][1] = o1;
-        } else if (MODE == SEL) {
-            nv[r][0] = (s.keep0 & (1u << r)) ? c0 : o0;
-            nv[r][1] = (s.keep1 & (1u << r)) ? c1 : o1;
-        } else if (MODE == MASK) {
+        } else {
             const uint32_t kall = (k < 1 || k > p.nk) ? 0xffffffffu : 0u;  // CTA-uniform
             nv[r][0] = ((s.keep0 | kall) & (1u << r)) ? c0 : o0;
             nv[r][1] = ((s.keep1 | kall) & (1u << r)) ? c1 : o1;
-        } else {
-            const int jr = dj + r, need = T - L;
-            const bool compute = (jr >= -need) && (jr < C::TJ + need) && (k >= 1) &&
-                                 (k <= p.nk) && (gj + r >= 1) && (gj + r <= p.nj);
-            // halo rows/planes keep their value; rows outside the trapezoid: anything
-            nv[r][0] = (compute && in_i0) ? o0 : c0;
-            nv[r][1] = (compute && in_i1) ? o1 : c1;
         }
     }
 }
@@ -423,13 +358,12 @@ __device__ __forceinline__ void level_finish(const double (&cc)[C::RJ][2],
 // three input planes straight from the TMA ring (slots g-2, g-1, g);
 // otherwise from register queue Q[0], fed from ring slot g.
 //
-// FAST steps run in two phases.  Phase 1 forms every level's partial sum P
+// Steps run in two phases.  Phase 1 forms every level's partial sum P
 // from data of the previous step only (centre and lower planes in registers, neighbour rows in
 // the exchange buffers / ring) -- T x RJ x 2 independent chains, so the
 // shuffles and adds of all levels overlap.  P overwrites the lower plane,
 // which nothing else needs.  Phase 2 is the short dependent chain through the
-// levels: level L's new plane is level L+1's U.  (SEL/SLOW steps keep the
-// one-pass form: their masks made the two-phase code longer than it gained.)
+// levels: level L's new plane is level L+1's U.
 template <class C, int MODE, bool AZ, int PH, bool PEER>
 __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CUtensorMap* dst_map,
                                             const JacobiParams& p,
@@ -457,9 +391,6 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
     const double* prv = ring + size_t(slot >= 1 ? slot - 1 : slot + S - 1) * C::BOXS;
     const double* pp = ring + size_t(slot >= 2 ? slot - 2 : slot + S - 2) * C::BOXS;
     const int pplane = it.kb - T + s.n;
-    const int gi = it.I0 + di, gj = it.J0 + dj;
-    const bool in_i0 = (gi >= 1) && (gi <= p.ni);
-    const bool in_i1 = (gi + 1 >= 1) && (gi + 1 <= p.ni);
     const double a = p.a, b = p.b;
 
     // emits level L's new plane: exchange rows + queue (L < T) or output
@@ -513,7 +444,7 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
         cen[RJ + 1][1] = n2.y;
     };
 
-    if constexpr (MODE == FAST || MODE == MASK) {
+    {
         // ---- phase 1: partial sums of every level (previous-step data) ----
         double P1[RJ][2], C1[RJ][2];  // L1S: level 1's P and centre plane (else unused)
 #pragma unroll
@@ -555,8 +486,7 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
         for (int L = 1; L <= T; ++L) {
             double nv[RJ][2];
             if (C::L1S && L == 1) {
-                level_finish<C, MODE, AZ>(C1, P1, U1, nv, a, b, L, dj, pplane - L, gj, in_i0,
-                                          in_i1, p, s);
+                level_finish<C, MODE, AZ>(C1, P1, U1, nv, a, b, pplane - L, p, s);
             } else {
                 LevelQ<C>& In = Q[C::L1S ? L - 2 : L - 1];
                 if (L == 1) {
@@ -566,53 +496,7 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
                         In.q[U][r][1] = U1[r][1];
                     }
                 }
-                level_finish<C, MODE, AZ>(In.q[CC], In.q[D], In.q[U], nv, a, b, L, dj,
-                                          pplane - L, gj, in_i0, in_i1, p, s);
-            }
-            emit(L, nv);
-        }
-    } else {
-        // SEL / SLOW: one pass per level
-        mbar_wait(&full[slot], phase);
-        if (!C::L1S) {
-#pragma unroll
-            for (int r = 0; r < RJ; ++r) {
-                const double2 x = lds2(cur + (brow + r) * BW + col);
-                Q[0].q[U][r][0] = x.x;
-                Q[0].q[U][r][1] = x.y;
-            }
-        }
-#pragma unroll
-        for (int L = 1; L <= T; ++L) {
-            const int k = pplane - L;
-            double nv[RJ][2];
-            double cen[RJ + 2][2];
-            nbr_rows(L, cen);
-            if (C::L1S && L == 1) {
-                double dn[RJ][2], up[RJ][2];
-#pragma unroll
-                for (int r = 0; r < RJ; ++r) {
-                    const double2 x = lds2(prv + (brow + r) * BW + col);
-                    const double2 y = lds2(pp + (brow + r) * BW + col);
-                    const double2 z = lds2(cur + (brow + r) * BW + col);
-                    cen[r + 1][0] = x.x;
-                    cen[r + 1][1] = x.y;
-                    dn[r][0] = y.x;
-                    dn[r][1] = y.y;
-                    up[r][0] = z.x;
-                    up[r][1] = z.y;
-                }
-                level_update<C, MODE, AZ>(cen, dn, up, nv, a, b, L, dj, k, gj, in_i0, in_i1, p,
-                                          s);
-            } else {
-                LevelQ<C>& In = Q[C::L1S ? L - 2 : L - 1];
-#pragma unroll
-                for (int r = 0; r < RJ; ++r) {
-                    cen[r + 1][0] = In.q[CC][r][0];
-                    cen[r + 1][1] = In.q[CC][r][1];
-                }
-                level_update<C, MODE, AZ>(cen, In.q[D], In.q[U], nv, a, b, L, dj, k, gj, in_i0,
-                                          in_i1, p, s);
+                level_finish<C, MODE, AZ>(In.q[CC], In.q[D], In.q[U], nv, a, b, pplane - L, p, s);
             }
             emit(L, nv);
         }
@@ -740,7 +624,8 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
         // Steps [n_lo, n_hi) compute interior planes only (step n computes
         // planes kb-T+n-L for L = 1..T; only the first/last steps of items
         // touching the k boundary are outside).  They run FAST when the
-        // tile's rows and columns lie inside [1,nj] x [1,ni], else SEL.
+        // tile's rows and columns lie inside [1,nj] x [1,ni]; every other
+        // step runs MASK.
         const int jlo = s.it.J0 - (T - 1);  // the tile's first computed row
         const bool ij_in = (s.it.I0 - C::H >= 1) && (s.it.I0 - C::H + C::BW - 1 <= p.ni) &&
                            (jlo >= 1) && (jlo + C::ROWS - 1 <= p.nj);
@@ -749,15 +634,15 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
         if constexpr (C::UNI) {
             jacobi_steps<C, MASK, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, s.it.N);
         } else {
-            jacobi_steps<C, SLOW, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, n_lo);
+            jacobi_steps<C, MASK, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, n_lo);
             if (ij_in)
                 jacobi_steps<C, FAST, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
-                                          n_hi - n_lo);
+                                                n_hi - n_lo);
             else
-                jacobi_steps<C, SEL, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
-                                         n_hi - n_lo);
-            jacobi_steps<C, SLOW, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
-                                      s.it.N - n_hi);
+                jacobi_steps<C, MASK, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
+                                                n_hi - n_lo);
+            jacobi_steps<C, MASK, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
+                                            s.it.N - n_hi);
         }
         s.n = 0;
         __syncthreads();  // queue[] entry written by thread 0 at least one barrier ago

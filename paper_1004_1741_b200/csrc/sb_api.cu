@@ -257,7 +257,7 @@ __global__ void fp64_probe_kernel(double* sink, int64_t iters) {
 // temporally blocked launch
 
 // Per tile: 1 if the tile's computed region touches the i/j boundary (its
-// interior steps run in SEL mode; jacobi_tb.cuh, the kernel's ij_in).
+// interior steps run in MASK mode; jacobi_tb.cuh, the kernel's ij_in).
 template <class C>
 static std::vector<char> border_tiles(int ni, int nj, int tiles_i, int tiles_j) {
     std::vector<char> v(size_t(tiles_i) * tiles_j);

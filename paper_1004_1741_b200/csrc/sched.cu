@@ -123,7 +123,7 @@ int pick_kblock(int T, int tiles, int nkout, int grid) {
 //      cut into m * grid k-pieces (m = SB_LIST_M or the model's best)
 //   2: (rounds - 1) bulk rounds, then the remaining tiles k-block-major with
 //      the block length the model picks (SB_LIST_KB overrides)
-// Border tiles (SEL step mode) cost SB_SELF (default 1.2) x a FAST tile.
+// Border tiles (MASK step mode) cost SB_SELF (default 1.2) x a FAST tile.
 static std::vector<Item> build_list(int mode, int T, int tiles_i, int tiles_j,
                                     const std::vector<char>& border, int kfirst, int klast,
                                     int grid, int m_or_kb) {
