@@ -564,6 +564,25 @@ __device__ __forceinline__ void jacobi_steps(const CUtensorMap* src_map, const C
     }
 }
 
+// The same from a step with g mod 3 == 0: no prologue, so each step
+// variant is inlined once per call site (the kernel's instruction-cache
+// footprint matters: profiles/r2/ab_phase_aligned.log).
+template <class C, int MODE, bool AZ, bool PEER>
+__device__ __forceinline__ void jacobi_steps0(const CUtensorMap* src_map, const CUtensorMap* dst_map,
+                                              const JacobiParams& p,
+                                              double* ring, double* xb, uint64_t* full,
+                                              ItemInfo* queue, LevelQ<C> (&Q)[C::NQ],
+                                              JState& s, int count) {
+    while (count > 0) {
+        jacobi_step<C, MODE, AZ, 0, PEER>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
+        if (--count == 0) return;
+        jacobi_step<C, MODE, AZ, 1, PEER>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
+        if (--count == 0) return;
+        jacobi_step<C, MODE, AZ, 2, PEER>(src_map, dst_map, p, ring, xb, full, queue, Q, s);
+        --count;
+    }
+}
+
 template <class C, bool AZ, bool PEER = false>
 __global__ void __launch_bounds__(C::NT, C::MINB)
 jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
@@ -634,15 +653,16 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
         if constexpr (C::UNI) {
             jacobi_steps<C, MASK, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, s.it.N);
         } else {
-            jacobi_steps<C, MASK, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, n_lo);
-            if (ij_in)
-                jacobi_steps<C, FAST, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
-                                                n_hi - n_lo);
-            else
-                jacobi_steps<C, MASK, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
-                                                n_hi - n_lo);
-            jacobi_steps<C, MASK, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
-                                            s.it.N - n_hi);
+            // MASK (exact on any step) up to the first step with g mod 3 == 0
+            // at or after n_lo, then FAST in whole rotations, then MASK: the
+            // FAST and tail loops start at phase 0 and need no prologue
+            int n1 = s.it.N;
+            if (ij_in) n1 = min(s.it.N, n_lo + int((3u - (s.g + n_lo) % 3u) % 3u));
+            jacobi_steps<C, MASK, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, n1);
+            const int nf = max(0, n_hi - n1) / 3 * 3;
+            jacobi_steps0<C, FAST, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s, nf);
+            jacobi_steps0<C, MASK, AZ, PEER>(&src_map, &dst_map, p, ring, xb, full, queue, Q, s,
+                                             s.it.N - n1 - nf);
         }
         s.n = 0;
         __syncthreads();  // queue[] entry written by thread 0 at least one barrier ago
