@@ -114,6 +114,7 @@ struct JacobiCfg {
     static constexpr int BOX = BW * BH;
     static constexpr int BOXS = (BOX + 15) / 16 * 16;  // 128-B aligned TMA destinations
     static constexpr int NT = NW * 32;
+    static constexpr int STORER = (NW - 1) * 32;       // thread issuing the output TMA stores
     static constexpr int XROW = 2 * BW;                // exchange doubles per warp: top + bottom row
     static constexpr int NX = (T > 1) ? (T - 1) : 0;   // levels with exchange rows (1..T-1)
     static constexpr int XSLOT = NW;                   // one slot per warp
@@ -506,7 +507,7 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
         fence_proxy_async_smem();  // staged rows -> visible to the TMA store
         // the store issued last step has read the other staging buffer, which
         // the next step overwrites
-        if (tid == 0) bulk_wait_read<0>();
+        if (tid == C::STORER) bulk_wait_read<0>();
     }
     __syncthreads();
     // fused halo exchange: an edge output plane, staged in shared memory, is
@@ -518,15 +519,16 @@ __device__ __forceinline__ bool jacobi_step(const CUtensorMap* src_map, const CU
         if (out_step) peer_copy<C>(p, ring + C::STG_OFF + (s.g & 1) * C::STG, it.I0, it.J0,
                                    it.kb - 2 * T + s.n);
     }
-    if (tid == 0) {
-        if (C::TS && out_step) {
-            tma_store_3d(dst_map, ring + C::STG_OFF + (s.g & 1) * C::STG, it.I0, it.J0,
-                         it.kb - 2 * T + s.n);
-            bulk_commit();
-        }
-        // the oldest ring slot (g-2 with L1S, else g-1) is free now: refill it
-        produce<C>(src_map, p, ring, full, queue);
+    // the per-step TMA duties after the barrier delay the warps that carry
+    // them into the next step (and so, through the next barrier, everyone):
+    // the output store goes to the last warp, the loads to warp 0
+    if (C::TS && out_step && tid == C::STORER) {
+        tma_store_3d(dst_map, ring + C::STG_OFF + (s.g & 1) * C::STG, it.I0, it.J0,
+                     it.kb - 2 * T + s.n);
+        bulk_commit();
     }
+    // the oldest ring slot (g-2 with L1S, else g-1) is free now: refill it
+    if (tid == 0) produce<C>(src_map, p, ring, full, queue);
     ++s.g;
     if (!POW2 && ++s.slot == S) {
         s.slot = 0;
@@ -669,7 +671,7 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
         s.cq = (s.cq + 1) % C::QSLOTS;
         s.it = queue[s.cq];
     }
-    if (C::TS && tid == 0) bulk_wait<0>();  // every output plane written before exit
+    if (C::TS && tid == C::STORER) bulk_wait<0>();  // every output plane written before exit
 }
 
 }  // namespace sb
