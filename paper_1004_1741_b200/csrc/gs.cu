@@ -1063,6 +1063,11 @@ int gs_slabs_fused(int nslabs, const int* devices, double* const* grids, const i
     }
     for (auto& m : members)
         if ((int)m.size() > kGsMaxSlabs) return SB_ERR_PLAN;
+    // the storer warps push into the neighbours' memory: neighbouring slabs on
+    // different GPUs need peer access (else the launch-per-sweep pipeline,
+    // whose ghost copies go through cudaMemcpyPeerAsync, runs)
+    for (int g = 0; g + 1 < nslabs; ++g)
+        if (!peer_reachable(devices[g], devices[g + 1])) return SB_ERR_PLAN;
     const int tiles_j = (nj + C::BJ - 1) / C::BJ;
     const size_t gbytes = size_t(C::R) * tiles_j * sizeof(int);
     std::vector<int> kt(nslabs);

@@ -37,6 +37,16 @@ struct HostCtx {
 static std::mutex g_host_mu;
 static HostCtx g_host[64];
 
+// true when kernels on device a can store into device b's memory (the same
+// device, or peer access possible both ways)
+bool peer_reachable(int a, int b) {
+    if (a == b) return true;
+    int ab = 0, ba = 0;
+    cudaDeviceCanAccessPeer(&ab, a, b);
+    cudaDeviceCanAccessPeer(&ba, b, a);
+    return ab && ba;
+}
+
 // partition_blocks semantics (reference sweeps/plan.py:106-120)
 static void part(int64_t extent, int count, int idx, int64_t* lo, int64_t* hi) {
     const int64_t base = extent / count, rem = extent % count;
@@ -379,9 +389,13 @@ int sb_jacobi_slabs(int nslabs, const int* devices, double* const* slabs, double
     // p-1 of s-1 and s+1: its ghosts were written there, and they read the
     // planes this period's edge launches overwrite.  Events alternate by
     // period parity so that a wait never lands on the same period.
+    // (the kernels store into the neighbours' buffers: slabs on different
+    // GPUs need peer access between them, else the copy-based exchange runs)
     bool fused = (ni % 2 == 0);
-    for (int s = 0; s < nslabs; ++s)
+    for (int s = 0; s < nslabs; ++s) {
         fused = fused && tma_ok(S[s].buf[0], ni) && tma_ok(S[s].buf[1], ni);
+        if (s + 1 < nslabs) fused = fused && peer_reachable(S[s].dev, S[s + 1].dev);
+    }
     if (fused) {
         std::vector<cudaEvent_t> pev[2];
         for (int par = 0; par < 2; ++par) {

@@ -67,6 +67,7 @@ int gs_run(double* grid, int ni, int nj, int nk, int64_t iters, double b, int ke
 int gs_slabs_fused(int nslabs, const int* devices, double* const* grids, const int64_t* nks, int ni,
                    int nj, int64_t iters, double b, int kernel, void* const* streams);
 int gs_check_error(cudaStream_t st);
+bool peer_reachable(int a, int b);  // kernels on a may store into b's memory
 
 // work schedules of the temporally blocked Jacobi launch (sched.cu)
 int64_t schedule_span(int T, int tiles, int nkout, int grid, int kb);
