@@ -86,8 +86,13 @@ def test_slab_layout_ghosts():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nslabs,depth,iters", [(2, 2, 7), (3, 4, 9), (4, 1, 5), (2, 8, 16)])
+@pytest.mark.parametrize("nslabs,depth,iters", [(2, 2, 7), (3, 4, 9), (4, 1, 5), (2, 8, 16),
+                                                (10, 4, 11), (5, 8, 13)])
 def test_c_abi_slabs_on_one_gpu(nslabs, depth, iters):
+    """sb_jacobi_slabs, every slab on GPU 0 with its own stream (the fused
+    exchange: edge launches store into the neighbours' ghost planes; the last
+    two cases have slabs exactly `depth` planes thick, so every owned plane
+    goes to both neighbours, and a shallower final period) == the oracle."""
     import ctypes
 
     import torch
