@@ -124,3 +124,20 @@ def test_config4_strong_through_run_vs_reference_hash(hashed_cases):
               g, devices=[0, 0])
     assert sha(out.data) == rec["output_sha256"]
     _lib.release_caches(0)
+
+
+def test_more_slabs_than_one_launch_takes_and_bad_devices():
+    """9 GS slabs on one GPU exceed one fused launch (8): the launch-per-
+    sweep pipeline runs instead, same bits; an invisible device index is a
+    ValueError before any work."""
+    from paper_1004_1741_b200.grid import InitPattern, create_grid
+
+    g = create_grid(20, 18, 27, InitPattern.seeded_random(8, -1.0, 1.0))
+    want = oracle.run_serial("gs-naive", g.data.copy(), 4, 0.0, 1 / 6)
+    out = run(SweepPlan("gs-naive", "pipeline", 4), g, devices=[0] * 9)
+    assert np.array_equal(out.data, want)
+    h = create_grid(20, 18, 27, InitPattern.seeded_random(8))
+    before = h.data.copy()
+    with pytest.raises(ValueError):
+        run(SweepPlan("jacobi", "threaded", 2), h, devices=[0, torch.cuda.device_count() + 3])
+    assert np.array_equal(h.data, before)
