@@ -351,7 +351,7 @@ def time_jacobi_depths(torch, lib, n, iters, depths):
                         "sweeps_fused_per_pass": min(d, 4),
                         "x_single_sweep_roofline": mlups * 1e6 * 16 / (PEAKS["hbm_gbs"] * 1e9)}
     # sb_jacobi fuses at most 4 sweeps per pass (deeper requests run as
-    # 4-sweep passes: the fastest on B200).  The genuinely 8-deep kernel (the
+    # 4-sweep passes).  The genuinely 8-deep kernel (the
     # slab path's ghost-zone block, sb_jacobi_planes) over the whole grid:
     sweeps = 8 * (iters // 8)
     bufs = (g, s)

@@ -106,9 +106,9 @@ int sb_jacobi_schedule(int sweeps, int64_t ni, int64_t nj, int64_t k_out_lo, int
  * pointers to two distinct padded grids; `scratch` needs no initialisation
  * (its halo is copied from `grid` on the stream).  Advances `iters` sweeps,
  * fusing up to `depth` (1..sb_max_depth()) sweeps per HBM pass (depths
- * above 4 run as 4-sweep passes, the fastest fused depth on B200; results
- * are identical for every depth); iters that are not a multiple of the
- * pass depth end with a shallower pass.  On return
+ * above 4 run as 4-sweep passes: sustained under the board power cap, 4 is
+ * the fastest fused depth on B200; results are identical for every depth);
+ * iters that are not a multiple of the pass depth end with a shallower pass.  On return
  * *result_in_scratch tells which buffer holds the final field (the other
  * holds an intermediate one), like run_serial returning the copy for odd
  * iteration counts.  Asynchronous on `stream`.

@@ -127,6 +127,7 @@ struct JacobiCfg {
     static constexpr size_t DBL_END = STG_OFF + (TS ? 2 * size_t(STG) : 0);
     // doubles, then queue[QSLOTS], mbarriers full[S], then the producer state
     static constexpr size_t SMEM_BYTES = DBL_END * 8 + 16 * QSLOTS + 8 * S + 32 + 64;
+    static_assert(SMEM_BYTES <= 232448, "tile configuration exceeds 227 KB of shared memory");
     static constexpr uint32_t BOX_BYTES = uint32_t(BOX) * 8;
 };
 

@@ -396,18 +396,33 @@ static int with_cfg(int T, F&& f) {
             if (v == 10) SB_L(3, 4, 8, 8, 1, false, true, true);
             if (v == 11) SB_L(3, 5, 8, 6, 1, false, true, true);
             if (v == 12) SB_L(3, 6, 8, 5, 1, false, true, true);
+            if (v == 13) SB_L(3, 6, 8, 5, 1, false, true);
+            if (v == 14) SB_L(3, 5, 8, 7, 1, false, true);
+            if (v == 16) SB_L(3, 6, 8, 6, 1, false, true);
+            if (v == 17) SB_L(3, 6, 8, 4, 1, false, true);
             break;
         case 4:
             if (v == 10) SB_L(4, 4, 8, 8, 1, false, true, true);
             if (v == 11) SB_L(4, 5, 8, 6, 1, false, true, true);
             if (v == 12) SB_L(4, 5, 8, 5, 1, false, true, true);
+            if (v == 15) SB_L(4, 5, 8, 6, 1, true, true);
+            break;
+        case 2:
+            if (v == 20) SB_L(2, 6, 8, 6, 1, false, true);
+            if (v == 21) SB_L(2, 8, 8, 4, 1, false, true);
+            if (v == 22) SB_L(2, 7, 8, 6, 1, false, true);
+            if (v == 23) SB_L(2, 6, 8, 5, 1, false, true);
             break;
     }
 #endif
     switch (T) {
         case 1: SB_L(1, 4, 8, 4, 2, false, true);
-        case 2: SB_L(2, 4, 8, 8, 1, false, true);
-        case 3: SB_L(3, 4, 8, 8, 1, false, true);
+        // T = 2, 3: 6 rows per thread (64 x 48 tiles) -- registers allow it at
+        // these depths; taller tiles cut the j-overlap (round 2: T=2 647 -> 709
+        // GLUP/s at 1024^3, 663 -> 730 at 512^3; T=3 783 -> 845, 717 -> 808;
+        // profiles/r2/ab_t2_t3_tall_tiles.log)
+        case 2: SB_L(2, 6, 8, 6, 1, false, true);
+        case 3: SB_L(3, 6, 8, 5, 1, false, true);
         case 4: SB_L(4, 4, 8, 8, 1, false, true);
         // depths 5-8 (the slab path's ghost-zone blocks, the config-3 "steps
         // per HBM pass" sweep): 12 warps x 2 rows; level 1 reads the TMA
