@@ -410,7 +410,6 @@ static int with_cfg(int T, F&& f) {
         case 2:
             if (v == 20) SB_L(2, 6, 8, 6, 1, false, true);
             if (v == 21) SB_L(2, 8, 8, 4, 1, false, true);
-            if (v == 22) SB_L(2, 7, 8, 6, 1, false, true);
             if (v == 23) SB_L(2, 6, 8, 5, 1, false, true);
             break;
     }
