@@ -449,11 +449,13 @@ def run_gpu_arm(args):
     avg = sum(s for _, s in full) / max(1, len(full))
     algo_bytes = 16.0 * cells_per_gpu
     achieved = algo_bytes / avg / 1e9 if avg > 0 else None
-    traffic = None
+    traffic = smem_wavefronts = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
     if tfile.exists():
         try:
-            traffic = json.loads(tfile.read_text()).get(f"jacobi_tb_T{depth}_1024")
+            ncu = json.loads(tfile.read_text())
+            traffic = ncu.get(f"jacobi_tb_T{depth}_1024")
+            smem_wavefronts = ncu.get(f"jacobi_tb_T{depth}_1024_smem_wavefronts")
         except Exception:  # noqa: BLE001
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": PEAKS["hbm_gbs"], "unit": "GB/s",
@@ -484,6 +486,20 @@ def run_gpu_arm(args):
     except Exception as exc:  # noqa: BLE001 -- a diagnostic; never fails the bench
         fp64 = {"error": str(exc)}
     roofline["fp64"] = fp64
+    # tertiary ceiling: the shared-memory pipe.  The kernel's
+    # shared-memory wavefronts per launch (shuffles, LDS/STS, TMA traffic) come
+    # from the committed ncu capture; the pipe retires one wavefront per SM and
+    # cycle, so its busy fraction follows from the launch time and SM clock
+    # measured in this run.
+    clocks = clk.summary()
+    if smem_wavefronts and avg > 0 and clocks.get("sm_mhz"):
+        peak_wf = torch.cuda.get_device_properties(local).multi_processor_count * clocks["sm_mhz"] * 1e6
+        roofline["smem"] = {"bound": "shared-memory pipe", "wavefronts_per_launch": smem_wavefronts,
+                            "achieved_wavefronts_per_s": smem_wavefronts / avg,
+                            "peak_wavefronts_per_s": peak_wf, "frac": smem_wavefronts / avg / peak_wf,
+                            "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum "
+                                      "(profiles/ncu_traffic.json), one wavefront per SM per cycle at the "
+                                      "SM clock sampled during the timed region"}
 
     # e2e through the public C-ABI host-buffer entry point: every step one
     # grid goes pinned host -> H2D -> SWEEPS sweeps -> D2H.  At N=1 the steps
@@ -538,7 +554,7 @@ def run_gpu_arm(args):
                         "zero Dirichlet halo)",
                 "config": arm_config(world, depth),
                 "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
-                "e2e": e2e, "clocks": clk.summary(), "also": also}
+                "e2e": e2e, "clocks": clocks, "also": also}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
