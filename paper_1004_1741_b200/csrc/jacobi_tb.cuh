@@ -90,6 +90,7 @@ struct JacobiCfg {
     // One loop instead of two leaves ptxas room for 5 rows per thread at
     // T = 4 without spilling.
     static constexpr bool UNI = UNI_;
+    static constexpr bool LISTONLY = T_ >= 3 && T_ != 4;  // see decode_item
     // TS: level T writes its output tile into a shared staging buffer (double
     // buffered) and one thread stores it with a TMA tensor store per plane,
     // instead of per-thread 16-byte global stores
@@ -154,7 +155,12 @@ __device__ __forceinline__ ItemInfo decode_item(const JacobiParams& p, int item)
         return it;
     }
     int t, ke;
-    if (p.list) {
+    // depths >= 3 always launch with an explicit list (sched.cu: item_list), so
+    // their kernels need no arithmetic decode (two integer divisions inlined
+    // at every item switch).  Dropping it changes ptxas' allocation: T=3 gains
+    // 1.7% at 512^3, T=4 loses 0.6% (32 instead of 8 spill bytes), so the
+    // T=4 kernel keeps both forms (profiles/r2/ab_list_only_decode.log).
+    if (C::LISTONLY || p.list) {
         const int4 v = __ldg(p.list + item);
         t = v.x;
         it.kb = v.y;
@@ -233,10 +239,12 @@ struct JState {      // per-thread loop state shared by the step functions
 };
 
 // The TMA producer's state.  Only thread 0 produces, so it lives in shared
-// memory instead of occupying registers in every thread.
-struct Prod {
+// memory instead of occupying registers in every thread: two 16-byte records
+// (counters, current item), each read with one load per step.
+struct alignas(16) Prod {
     uint32_t ld_issued;  // plane loads issued
     int pq, pn;          // queue slot / plane step of the producer's item
+    int pad;
     ItemInfo pitem;      // producer's item
 };
 
@@ -274,26 +282,40 @@ __device__ __forceinline__ void next_item(const JacobiParams& p, ItemInfo* queue
     queue[pr.pq] = pr.pitem;
 }
 
+// Prod sits between the item queue and the mbarriers (16-byte aligned).
 template <class C>
-__device__ __forceinline__ Prod* prod_state(uint64_t* full) {
-    return reinterpret_cast<Prod*>(full + C::S);
+__device__ __forceinline__ Prod* prod_state(ItemInfo* queue) {
+    return reinterpret_cast<Prod*>(queue + C::QSLOTS);
 }
 
+// One plane load of the producer's item into the ring slot of load number
+// ld_issued.  The whole state is read up front (two independent 16-byte
+// shared loads) and kept in registers across the mbarrier / TMA
+// instructions: thread 0 carries this after every step barrier, and every
+// dependent shared-memory round trip here delays warp 0 -- and, through the
+// next barrier, the CTA.
 template <class C>
 __device__ __forceinline__ void produce(const CUtensorMap* src_map, const JacobiParams& p,
                                         double* ring, uint64_t* full, ItemInfo* queue) {
     constexpr int S = C::S;
-    Prod& pr = *prod_state<C>(full);
-    if (pr.pitem.N <= 0) return;
-    uint64_t* bar = &full[pr.ld_issued % S];
+    Prod& pr = *prod_state<C>(queue);
+    const int4 cnt = *reinterpret_cast<const int4*>(&pr);         // ld_issued, pq, pn, -
+    const int4 itm = *reinterpret_cast<const int4*>(&pr.pitem);  // I0, J0, kb, N
+    if (itm.w <= 0) return;
+    const uint32_t ld = uint32_t(cnt.x);
+    const int slot = int(ld % S);
+    uint64_t* bar = &full[slot];
     mbar_arrive_expect_tx(bar, C::BOX_BYTES);
-    tma_load_3d(ring + size_t(pr.ld_issued % S) * C::BOXS, src_map, pr.pitem.I0 - C::H,
-                pr.pitem.J0 - C::T, pr.pitem.kb - C::T + pr.pn, bar);
-    ++pr.ld_issued;
-    if (++pr.pn == pr.pitem.N) {
+    tma_load_3d(ring + size_t(slot) * C::BOXS, src_map, itm.x - C::H, itm.y - C::T,
+                itm.z - C::T + cnt.z, bar);
+    if (cnt.z + 1 == itm.w) {
+        pr.ld_issued = ld + 1;
         pr.pn = 0;
-        pr.pq = (pr.pq + 1) % C::QSLOTS;
+        pr.pq = (cnt.y + 1) % C::QSLOTS;
         next_item<C>(p, queue, pr);
+    } else {
+        pr.ld_issued = ld + 1;
+        pr.pn = cnt.z + 1;
     }
 }
 
@@ -594,9 +616,9 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
     extern __shared__ __align__(128) double smem[];
     double* ring = smem + C::RING_OFF;
     double* xb = smem + C::X_OFF;
-    // queue[QSLOTS] (16-byte entries, 128-byte aligned), full[S], qbar[QSLOTS]
+    // queue[QSLOTS] (16-byte entries, 128-byte aligned), the producer state, full[S]
     ItemInfo* queue = reinterpret_cast<ItemInfo*>(smem + C::DBL_END);
-    uint64_t* full = reinterpret_cast<uint64_t*>(queue + C::QSLOTS);
+    uint64_t* full = reinterpret_cast<uint64_t*>(prod_state<C>(queue) + 1);
     const int tid = threadIdx.x;
 
     JState s;
@@ -607,7 +629,7 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src_map,
         fence_mbar_init();
     }
     if (tid == 0) {
-        Prod& pr = *prod_state<C>(full);
+        Prod& pr = *prod_state<C>(queue);
         pr.ld_issued = 0;
         pr.pq = pr.pn = 0;
         next_item<C>(p, queue, pr);

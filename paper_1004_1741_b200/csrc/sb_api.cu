@@ -339,16 +339,15 @@ static int launch_tb_impl(const double* src, double* dst, int ni, int nj, int nk
     p.kblocks = (nkout + kb - 1) / kb;
     p.items = tiles * p.kblocks;
     p.list = nullptr;
-    if (pl.list_ok) {
+    if (C::T >= 3) {  // explicit item list (always: these kernels decode no other form)
         const int4* list;
         int count;
         if ((rc = item_list(C::T, p.tiles_i, p.tiles_j, border_tiles<C>(ni, nj, p.tiles_i, p.tiles_j),
-                            kfirst, klast, grid, kb, &list, &count)))
+                            kfirst, klast, grid, kb, !pl.list_ok, &list, &count)))
             return rc;
-        if (list) {
-            p.list = list;
-            p.items = count;
-        }
+        if (!list) return fail(SB_ERR_PLAN, "no item list for depth %d", C::T);
+        p.list = list;
+        p.items = count;
     }
     p.a = a;
     p.b = b;

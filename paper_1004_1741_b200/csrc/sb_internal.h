@@ -75,7 +75,7 @@ int pick_kblock(int T, int tiles, int nkout, int grid);
 std::vector<int4> build_item_list(int T, int tiles_i, int tiles_j, const std::vector<char>& border,
                                   int kfirst, int klast, int grid, int kb);
 int item_list(int T, int tiles_i, int tiles_j, const std::vector<char>& border, int kfirst,
-              int klast, int grid, int kb, const int4** out, int* count);
+              int klast, int grid, int kb, bool regular_only, const int4** out, int* count);
 
 // free the per-device buffers kept between calls; true if there were any
 bool gs_release(int dev);

@@ -213,24 +213,32 @@ std::vector<int4> build_item_list(int T, int tiles_i, int tiles_j, const std::ve
 }
 
 int item_list(int T, int tiles_i, int tiles_j, const std::vector<char>& border, int kfirst,
-              int klast, int grid, int kb, const int4** out, int* count) {
+              int klast, int grid, int kb, bool regular_only, const int4** out, int* count) {
     *out = nullptr;
     *count = 0;
     const int mode = env_int("SB_LIST", 1);
-    if (T < 3 || mode == 0) return SB_OK;
+    if (T < 3) return SB_OK;  // T = 1, 2: short regular k-blocks, decoded arithmetically
     int dev;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     static std::mutex mu;
-    static std::map<std::tuple<int, int, int, int, int, int, int, int, std::vector<char>>,
+    static std::map<std::tuple<int, int, int, int, int, int, int, int, int, std::vector<char>>,
                     std::pair<int4*, int>>
         cache;
-    const auto key = std::make_tuple(dev, T, tiles_i, tiles_j, kfirst, klast, grid, mode, border);
+    const auto key = std::make_tuple(dev, T, tiles_i, tiles_j, kfirst, klast, grid,
+                                     regular_only ? -1 : mode, kb, border);
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
     if (it == cache.end()) {
-        const std::vector<int4> h =
-            build_item_list(T, tiles_i, tiles_j, border, kfirst, klast, grid, kb);
+        std::vector<int4> h;
+        if (!regular_only) h = build_item_list(T, tiles_i, tiles_j, border, kfirst, klast, grid, kb);
+        // where the model prefers the regular decomposition it is uploaded as
+        // a list too, in claim order (k-block major): kernels of depth >= 3
+        // decode items from a list only
+        if (h.empty())
+            for (int k0 = kfirst; k0 < klast; k0 += std::max(kb, 1))
+                for (int t = 0; t < tiles_i * tiles_j; ++t)
+                    h.push_back(make_int4(t, k0, std::min(k0 + std::max(kb, 1), klast), 0));
         int4* d = nullptr;
         if (!h.empty()) {
             e = cudaMalloc(&d, h.size() * sizeof(int4));
