@@ -118,22 +118,38 @@ class SlabEngine:
             w.wait()
         self.pending = []
 
-    def period(self, sweeps):
-        """Advance `sweeps` (<= depth) sweeps; the exchange stays in flight
-        until the next period (or wait())."""
-        assert 1 <= sweeps <= self.depth
-        self.wait()
-        src, dst = self.bufs[self.cur], self.bufs[self.cur ^ 1]
+    def ranges(self):
+        """(edge_lo, edge_hi, interior) local plane ranges of one period: the
+        owned planes a neighbour's ghosts are fed from, and the rest."""
         lo, hi, d = self.glo, self.glo + self.n_own, self.depth
         inner_lo = min(lo + d, hi) if self.rank > 0 else lo
         inner_hi = max(hi - d, inner_lo) if self.rank + 1 < self.world else hi
+        return (lo, inner_lo), (inner_hi, hi), (inner_lo, inner_hi)
+
+    def edges(self, sweeps):
+        """Phase 1 of a period: the ghost-feeding edge planes, src -> dst."""
+        assert 1 <= sweeps <= self.depth
+        src, dst = self.bufs[self.cur], self.bufs[self.cur ^ 1]
+        (a0, a1), (b0, b1), _ = self.ranges()
         if self.rank > 0:
-            self.compute(src, dst, self.nkl, lo, inner_lo, sweeps)
+            self.compute(src, dst, self.nkl, a0, a1, sweeps)
         if self.rank + 1 < self.world:
-            self.compute(src, dst, self.nkl, inner_hi, hi, sweeps)
-        self.pending = list(self._exchange(dst)) if self.world > 1 else []
-        self.compute(src, dst, self.nkl, inner_lo, inner_hi, sweeps)
+            self.compute(src, dst, self.nkl, b0, b1, sweeps)
+
+    def interior(self, sweeps):
+        """Phase 3 of a period: the remaining owned planes; flips the buffers."""
+        src, dst = self.bufs[self.cur], self.bufs[self.cur ^ 1]
+        _, _, (c0, c1) = self.ranges()
+        self.compute(src, dst, self.nkl, c0, c1, sweeps)
         self.cur ^= 1
+
+    def period(self, sweeps):
+        """Advance `sweeps` (<= depth) sweeps; the exchange stays in flight
+        until the next period (or wait())."""
+        self.wait()
+        self.edges(sweeps)
+        self.pending = list(self._exchange(self.bufs[self.cur ^ 1])) if self.world > 1 else []
+        self.interior(sweeps)
 
     def run(self, iters):
         left = iters

@@ -142,6 +142,53 @@ def test_slab_engine_single_rank_matches_oracle():
     assert sha(eng.owned().cpu().numpy()) == sha(want[1:-1])
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,shape,iters,depth", [
+    (3, (62, 20, 36), 10, 4),
+    (2, (128, 70, 40), 9, 4),
+    (4, (254, 33, 50), 7, 3),
+    (2, (64, 40, 24), 16, 8),
+])
+def test_rank_engines_in_lockstep_on_one_gpu(world, shape, iters, depth):
+    """The bench's N > 1 compute path on real launches: `world` rank engines
+    (edge launches, ghost layout, interior launch through sb_jacobi_planes)
+    advance period by period on one GPU; the NCCL exchange is replaced by
+    copies of the same plane ranges between the engines."""
+    import torch
+
+    from paper_1004_1741_b200.slabs import SlabEngine, gpu_compute
+
+    spec = {"shape": list(shape), "pattern": "random", "seed": 9, "lo": -1.0, "hi": 1.0}
+    g = make_input(spec)
+    a, b = 0.25, 0.125
+    like = torch.empty(0, dtype=torch.float64, device="cuda")
+    engs = [SlabEngine(g.ni, g.nj, g.nk, depth, r, world, gpu_compute(g.ni, g.nj, a, b), like=like)
+            for r in range(world)]
+    for e in engs:
+        e.load_global(g.data)
+    left = iters
+    while left > 0:
+        t = min(depth, left)
+        for e in engs:
+            e.edges(t)
+        for r, e in enumerate(engs):  # what SlabEngine._exchange sends and receives
+            dst, d, hi = e.bufs[e.cur ^ 1], e.depth, e.glo + e.n_own
+            if r + 1 < world:
+                up = engs[r + 1]
+                dst[hi:hi + d].copy_(up.bufs[up.cur ^ 1][up.glo:up.glo + d])
+            if r > 0:
+                dn = engs[r - 1]
+                dhi = dn.glo + dn.n_own
+                dst[0:e.glo].copy_(dn.bufs[dn.cur ^ 1][dhi - d:dhi])
+        for e in engs:
+            e.interior(t)
+        left -= t
+    torch.cuda.synchronize()
+    want = oracle.run_serial("jacobi", g.data, iters, a, b)
+    got = np.concatenate([e.owned().cpu().numpy() for e in engs])
+    assert sha(got) == sha(want[1:-1])
+
+
 # ---------------------------------------------------------------------------
 # Gauss-Seidel cross-slab pipeline
 
