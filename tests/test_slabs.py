@@ -318,6 +318,43 @@ def test_gs_slab_engine_single_rank_matches_oracle():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("world,shape,iters,kernel", [
+    (3, (62, 20, 36), 5, "gs-naive"),
+    (2, (128, 70, 40), 4, "gs-interleaved"),
+    (4, (30, 33, 50), 6, "gs-naive"),
+])
+def test_gs_rank_engines_in_pipeline_order_on_one_gpu(world, shape, iters, kernel):
+    """The torchrun GS engine's compute path on real launches: `world` rank
+    engines sweep their slabs (sb_gs on the local grid with its ghost planes)
+    in pipeline order on one GPU; the plane sends are replaced by copies."""
+    import torch
+
+    from paper_1004_1741_b200.slabs import GsSlabEngine, gpu_gs_compute
+
+    spec = {"shape": list(shape), "pattern": "random", "seed": 11, "lo": -1.0, "hi": 1.0}
+    g = make_input(spec)
+    b = 1 / 6
+    like = torch.empty(0, dtype=torch.float64, device="cuda")
+    engs = [GsSlabEngine(g.ni, g.nj, g.nk, r, world, gpu_gs_compute(g.ni, g.nj, b, kernel), like=like)
+            for r in range(world)]
+    for e in engs:
+        e.load_global(g.data)
+    for _ in range(iters):
+        for r, e in enumerate(engs):  # rank r's sweep s after rank r-1's sweep s
+            if r > 0:
+                dn = engs[r - 1]
+                e.grid[0].copy_(dn.grid[dn.nkl])          # new values of the plane below
+            if r + 1 < world:
+                up = engs[r + 1]
+                e.grid[e.nkl + 1].copy_(up.grid[1])       # old values of the plane above
+            e.compute(e.grid, e.nkl, 1)
+    torch.cuda.synchronize()
+    want = oracle.run_serial(kernel, g.data, iters, 0.0, b)
+    got = np.concatenate([e.owned().cpu().numpy() for e in engs])
+    assert sha(got) == sha(want[1:-1])
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("nslabs", [2, 8])
 def test_c_abi_gs_slabs_full_size(nslabs):
     """Config 5's shape (512^3, U[-1,1)): the GS z-pipeline over `nslabs`
