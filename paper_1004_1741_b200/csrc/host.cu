@@ -18,6 +18,7 @@
 #include <functional>
 #include <cstring>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "../../include/stencil_b200.h"
@@ -46,6 +47,38 @@ bool peer_reachable(int a, int b) {
     cudaDeviceCanAccessPeer(&ba, b, a);
     return ab && ba;
 }
+
+// Streams and events created for the duration of one driver call, destroyed
+// on every return path (error returns included).
+struct CallHandles {
+    std::vector<std::pair<int, cudaStream_t>> streams;
+    std::vector<std::pair<int, cudaEvent_t>> events;
+    cudaError_t stream(int dev, cudaStream_t* out) {
+        cudaError_t e = cudaSetDevice(dev);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);
+        if (e == cudaSuccess) streams.emplace_back(dev, *out);
+        return e;
+    }
+    cudaError_t event(int dev, cudaEvent_t* out) {
+        cudaError_t e = cudaSetDevice(dev);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(out, cudaEventDisableTiming);
+        if (e == cudaSuccess) events.emplace_back(dev, *out);
+        return e;
+    }
+    ~CallHandles() {
+        for (auto& x : events) {
+            cudaSetDevice(x.first);
+            cudaEventDestroy(x.second);
+        }
+        for (auto& x : streams) {
+            cudaSetDevice(x.first);
+            cudaStreamDestroy(x.second);
+        }
+    }
+    CallHandles() = default;
+    CallHandles(const CallHandles&) = delete;
+    CallHandles& operator=(const CallHandles&) = delete;
+};
 
 // partition_blocks semantics (reference sweeps/plan.py:106-120)
 static void part(int64_t extent, int count, int idx, int64_t* lo, int64_t* hi) {
@@ -359,7 +392,8 @@ int sb_jacobi_slabs(int nslabs, const int* devices, double* const* slabs, double
     const int64_t nip = ni + 2, plane = nip * (nj + 2);
     const size_t pbytes = size_t(plane) * sizeof(double);
     cudaError_t e;
-    // streams/events; peer access where the slabs live on different GPUs
+    CallHandles handles;  // this call's streams and events (DeviceGuard restores the device after it)
+    // peer access where the slabs live on different GPUs
     for (int s = 0; s < nslabs; ++s) {
         if ((e = cudaSetDevice(S[s].dev)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
         for (int t = 0; t < nslabs; ++t)
@@ -372,11 +406,6 @@ int sb_jacobi_slabs(int nslabs, const int* devices, double* const* slabs, double
                     else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
                 }
             }
-        if ((e = cudaStreamCreateWithFlags(&S[s].comm, cudaStreamNonBlocking)) != cudaSuccess)
-            return cuda_fail(e, "cudaStreamCreate");
-        for (cudaEvent_t* ev : {&S[s].edge, &S[s].start, &S[s].sent_up, &S[s].sent_dn})
-            if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
-                return cuda_fail(e, "cudaEventCreate");
         // both buffers must carry the Dirichlet halo (and the initial ghosts)
         if ((rc = halo_copy(S[s].buf[0], S[s].buf[1], (int)ni, (int)nj, (int)S[s].nkl, S[s].st))) return rc;
     }
@@ -400,11 +429,9 @@ int sb_jacobi_slabs(int nslabs, const int* devices, double* const* slabs, double
         std::vector<cudaEvent_t> pev[2];
         for (int par = 0; par < 2; ++par) {
             pev[par].assign(nslabs, nullptr);
-            for (int s = 0; s < nslabs; ++s) {
-                cudaSetDevice(S[s].dev);
-                if ((e = cudaEventCreateWithFlags(&pev[par][s], cudaEventDisableTiming)) != cudaSuccess)
+            for (int s = 0; s < nslabs; ++s)
+                if ((e = handles.event(S[s].dev, &pev[par][s])) != cudaSuccess)
                     return cuda_fail(e, "cudaEventCreate");
-            }
         }
         rc = SB_OK;
         int64_t period = 0;
@@ -455,12 +482,15 @@ int sb_jacobi_slabs(int nslabs, const int* devices, double* const* slabs, double
             cudaSetDevice(S[s].dev);
             if ((e = cudaStreamSynchronize(S[s].st)) != cudaSuccess && rc == SB_OK)
                 rc = cuda_fail(e, "slab sweeps");
-            cudaStreamDestroy(S[s].comm);
-            for (cudaEvent_t ev : {S[s].edge, S[s].start, S[s].sent_up, S[s].sent_dn}) cudaEventDestroy(ev);
-            for (int par = 0; par < 2; ++par) cudaEventDestroy(pev[par][s]);
         }
         *result_in_scratch = cur;
         return rc;
+    }
+    // copy-based exchange: a comm stream and four events per slab
+    for (int s = 0; s < nslabs; ++s) {
+        if ((e = handles.stream(S[s].dev, &S[s].comm)) != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+        for (cudaEvent_t* ev : {&S[s].edge, &S[s].start, &S[s].sent_up, &S[s].sent_dn})
+            if ((e = handles.event(S[s].dev, ev)) != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
     }
     bool first = true;
     for (int64_t done = 0; done < iters;) {
@@ -526,8 +556,6 @@ int sb_jacobi_slabs(int nslabs, const int* devices, double* const* slabs, double
         cudaSetDevice(S[s].dev);
         if ((e = cudaStreamSynchronize(S[s].comm)) != cudaSuccess) return cuda_fail(e, "exchange");
         if ((e = cudaStreamSynchronize(S[s].st)) != cudaSuccess) return cuda_fail(e, "slab sweeps");
-        cudaStreamDestroy(S[s].comm);
-        for (cudaEvent_t ev : {S[s].edge, S[s].start, S[s].sent_up, S[s].sent_dn}) cudaEventDestroy(ev);
     }
     *result_in_scratch = cur;
     return SB_OK;
@@ -623,12 +651,10 @@ int sb_gs_slabs(int nslabs, const int* devices, double* const* slabs, int64_t ni
     }
     // not eligible (odd ni, unaligned slabs, > 8 slabs on a device): one
     // sb_gs launch per slab and sweep, ghost planes copied between them
-    for (int g = 0; g < nslabs; ++g) {
-        cudaSetDevice(S[g].dev);
+    CallHandles handles;
+    for (int g = 0; g < nslabs; ++g)
         for (cudaEvent_t* ev : {&S[g].done, &S[g].got_lo, &S[g].got_hi})
-            if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
-                return cuda_fail(e, "cudaEventCreate");
-    }
+            if ((e = handles.event(S[g].dev, ev)) != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
     for (int64_t sw = 0; sw < iters; ++sw) {
         for (int g = 0; g < nslabs; ++g) {
             Slab& X = S[g];
@@ -662,7 +688,6 @@ int sb_gs_slabs(int nslabs, const int* devices, double* const* slabs, int64_t ni
         cudaSetDevice(S[g].dev);
         if ((e = cudaStreamSynchronize(S[g].st)) != cudaSuccess && rc == SB_OK)
             rc = cuda_fail(e, "slab sweeps");
-        for (cudaEvent_t ev : {S[g].done, S[g].got_lo, S[g].got_hi}) cudaEventDestroy(ev);
     }
     return rc;
 }
